@@ -1,0 +1,522 @@
+#!/usr/bin/env python
+"""Benchmark of the thread-transposed element-integration kernel on B200.
+
+Contract (one JSON line from rank 0):
+  metric   BASELINE.json's: element-integration GF/s (paper Eq. 7 flops), with
+           HBM GB/s and the roofline fraction in ``roofline``.
+  step     one integration pass over the workload's cells (one kernel launch).
+  workload 3D P1 tetrahedra, variable-coefficient Laplacian (P0 kappa), f64,
+           2^20 cells per GPU (BASELINE.json configs[1]); N GPUs own contiguous
+           cell ranges of an N*2^20-cell Kuhn mesh (weak scaling, no collective
+           on the data path).
+  value    whole-job GF/s, inputs resident in HBM; 4+ rotating buffer sets so
+           every step's inputs are out of L2 (set bytes x (sets-1) > 126 MB L2).
+  e2e      the same metric through the reference-facing call with HOST numpy
+           buffers (pinned): H2D + kernel + D2H inside the timed region.
+  --impl reference   the reference's own CPU lane (oracle/_ref/_kernels_cy,
+           built from /root/reference; else the C oracle port) on all host
+           cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+L2_BYTES = 126 * 1024 * 1024
+FALLBACK_HBM_GBS = 6650.0
+
+CONFIGS = {
+    # name: (dim, physics, dtype, cells per GPU)
+    "3d_varcoef_f64": (3, "varcoef_p0", "f64", 1 << 20),
+    "3d_varcoef_f32": (3, "varcoef_p0", "f32", 1 << 20),
+    "2d_varcoef_f64": (2, "varcoef_p0", "f64", 1 << 20),
+    "2d_varcoef_f32": (2, "varcoef_p0", "f32", 1 << 20),
+    "2d_varcoef_f64_65536": (2, "varcoef_p0", "f64", 65536),
+    "2d_elasticity_f64": (2, "elasticity", "f64", 1 << 20),
+    "2d_elasticity_f32": (2, "elasticity", "f32", 1 << 20),
+    "3d_elasticity_f64": (3, "elasticity", "f64", 1 << 20),
+    "3d_elasticity_f32": (3, "elasticity", "f32", 1 << 20),
+    "3d_varcoef_f32_2^24": (3, "varcoef_p0", "f32", 1 << 24),
+    "3d_varcoef_f64_2^24": (3, "varcoef_p0", "f64", 1 << 24),
+}
+HEADLINE = "3d_varcoef_f64"
+VARIANTS = ["3d_varcoef_f32", "2d_varcoef_f64", "2d_varcoef_f32", "2d_elasticity_f64", "2d_elasticity_f32",
+            "3d_elasticity_f64", "3d_elasticity_f32", "3d_varcoef_f32_2^24", "3d_varcoef_f64_2^24"]
+
+
+def peaks():
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy_)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def config_model(name):
+    from paper_1607_04245_b200.perf_model import compulsory_bytes_per_cell, flops_per_cell
+    from paper_1607_04245_b200.schedule import derive_execution_geometry
+
+    dim, physics, dtype, n = CONFIGS[name]
+    n_comp = dim if physics == "elasticity" else 1
+    width = 4 if dtype == "f32" else 8
+    aux = "p0" if physics == "varcoef_p0" else None
+    g = derive_execution_geometry(dim, dim + 1, n_comp, 1, 1, 1, n)
+    return flops_per_cell(g), compulsory_bytes_per_cell(dim, n_comp, width, aux)
+
+
+# ----------------------------------------------------------------------------
+# clocks during the timed region (NVML, polled from a thread)
+# ----------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], 0, False
+        self.max_mhz = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        names = [n for bit, n in self.REASONS.items() if self.reasons & bit and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------
+# GPU arm
+# ----------------------------------------------------------------------------
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def rank_workload(name, rank, world, seed=1234):
+    """Rank r's contiguous cell range of the N x cells-per-GPU Kuhn mesh, generated on its GPU."""
+    import torch
+
+    from paper_1607_04245_b200.mesh import CellGeometry, FieldLayout, Mesh, compute_geometry, \
+        gather_coefficients, generate_unit_simplex_mesh
+    from paper_1607_04245_b200.physics import CellAux
+    from paper_1607_04245_b200.shard import cell_range
+    from paper_1607_04245_b200.workload import PHYSICS, refine_for
+    from paper_1607_04245_b200.element import quadrature_rule, tabulate
+
+    dim, physics, dtype, per_gpu = CONFIGS[name]
+    total = per_gpu * world
+    lo, hi = cell_range(total, rank, world, align=256)
+    factory, aux_space = PHYSICS[physics]
+    form = factory(dim)
+    rule = quadrature_rule(dim, 1)
+    tab = tabulate(dim, rule)
+    full = generate_unit_simplex_mesh(dim, refine_for(dim, total))
+    cells_np = np.ascontiguousarray(full.cells[lo:hi])
+    cells = torch.from_numpy(cells_np).to("cuda")
+    sliced = Mesh(dim, full.vertices, cells_np)
+    geom = compute_geometry(sliced, cells=cells, device_out=True)
+    layout = FieldLayout(form.n_comp)
+    glob = np.random.default_rng(seed).standard_normal(layout.global_size(full))
+    coeffs = gather_coefficients(sliced, layout, torch.from_numpy(glob).to("cuda"), cells=cells)
+    tdt = torch.float32 if dtype == "f32" else torch.float64
+    aux = None
+    if aux_space == "p0":
+        vals = np.random.default_rng(seed + 1).uniform(0.5, 1.5, (full.n_cells, 1))[lo:hi]
+        aux = CellAux("p0", torch.from_numpy(np.ascontiguousarray(vals)).to("cuda", tdt))
+    c = lambda t: t.to(tdt).contiguous()  # noqa: E731
+    return dict(form=form, rule=rule, tab=tab, inv=c(geom.inv_jacobians), det=c(geom.determinants),
+                coeffs=c(coeffs), aux=aux, n=hi - lo, dtype=dtype, dim=dim)
+
+
+def time_device(wl, steps, warmup, n_sets, barrier=None, sampler=None):
+    """Device-resident timing: K launches rotating over n_sets buffer sets.
+
+    Returns (total_ms over the K steps, per-launch event durations in ms)."""
+    import torch
+
+    from paper_1607_04245_b200 import backend
+    from paper_1607_04245_b200.physics import CellAux
+
+    kernel = backend.cuda_kernel(wl["form"], wl["rule"].n_q, wl["aux"], 4 if wl["dtype"] == "f32" else 8)
+    sets = []
+    for _ in range(n_sets):
+        aux = None if wl["aux"] is None else CellAux("p0", wl["aux"].values.clone())
+        sets.append((wl["inv"].clone(), wl["det"].clone(), wl["coeffs"].clone(), aux,
+                     torch.empty_like(wl["coeffs"])))
+    tab, rule = wl["tab"], wl["rule"]
+    npdt = np.float32 if wl["dtype"] == "f32" else np.float64
+    B, D, W = (np.ascontiguousarray(x, dtype=npdt) for x in (tab.basis, tab.basis_der, rule.weights))
+
+    def launch(i):
+        inv, det, co, aux, out = sets[i % n_sets]
+        backend.run_cuda(kernel, B, D, W, inv, det, co, aux, out)
+
+    for i in range(warmup):
+        launch(i)
+    stream = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if barrier:
+        barrier()
+    torch.cuda.synchronize()
+    with (sampler if sampler else _null()):
+        t0.record(stream)
+        for i in range(steps):
+            ev[i][0].record(stream)
+            launch(warmup + i)
+            ev[i][1].record(stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    if barrier:
+        barrier()
+    total = t0.elapsed_time(t1)
+    per = [a.elapsed_time(b) for a, b in ev]
+    # the last set's result must match the first (same inputs): cheap self-check
+    assert torch.equal(sets[0][4], sets[(warmup + steps - 1) % n_sets][4]) or n_sets == 1
+    return total, per
+
+
+class _null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def time_e2e(wl, steps, warmup):
+    """Through the reference-facing call with HOST buffers (pinned numpy):
+    H2D + kernel + D2H per step inside the timed region (wall clock; the host
+    call returns only after the result is in host memory)."""
+    import torch
+
+    from paper_1607_04245_b200 import backend
+    from paper_1607_04245_b200.physics import CellAux
+
+    def pinned(t):
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t)
+        return h.numpy()
+
+    inv, det, co = pinned(wl["inv"]), pinned(wl["det"]), pinned(wl["coeffs"])
+    aux = None if wl["aux"] is None else CellAux("p0", pinned(wl["aux"].values))
+    out = torch.empty(tuple(co.shape), dtype=wl["coeffs"].dtype, pin_memory=True).numpy()
+    tab, rule = wl["tab"], wl["rule"]
+    kernel = backend.cuda_kernel(wl["form"], rule.n_q, wl["aux"], co.dtype.itemsize)
+    npdt = co.dtype
+    B, D, W = (np.ascontiguousarray(x, dtype=npdt) for x in (tab.basis, tab.basis_der, rule.weights))
+    for _ in range(warmup):
+        backend.run_cuda(kernel, B, D, W, inv, det, co, aux, out)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        backend.run_cuda(kernel, B, D, W, inv, det, co, aux, out)
+    dt = time.perf_counter() - t0
+    h2d = inv.nbytes + det.nbytes + co.nbytes + (aux.values.nbytes if aux is not None else 0)
+    return dt, h2d, out.nbytes, out
+
+
+def stream_probe(read_b, write_b, reps=20):
+    """Measured achievable HBM GB/s of a STREAM-like kernel at the kernel's read:write ratio."""
+    import ctypes
+
+    import torch
+
+    from paper_1607_04245_b200 import _lib
+
+    scale = 8
+    rb = (read_b * scale + 15) // 16 * 16
+    wb = (write_b * scale + 15) // 16 * 16
+    n_sets = 4
+    src = [torch.empty(rb, dtype=torch.uint8, device="cuda").fill_(1) for _ in range(n_sets)]
+    dst = [torch.empty(wb, dtype=torch.uint8, device="cuda") for _ in range(n_sets)]
+    s = torch.cuda.current_stream()
+    L = _lib.lib()
+    for i in range(3):
+        L.txb_stream_probe(src[i % n_sets].data_ptr(), rb, dst[i % n_sets].data_ptr(), wb,
+                           ctypes.c_void_p(s.cuda_stream))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(s)
+    for i in range(reps):
+        _lib.check(L.txb_stream_probe(src[i % n_sets].data_ptr(), rb, dst[i % n_sets].data_ptr(), wb,
+                                      ctypes.c_void_p(s.cuda_stream)))
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    return (rb + wb) / (ms * 1e-3) / 1e9
+
+
+# ----------------------------------------------------------------------------
+# CPU arm: the reference's compiled lane over a fork pool
+# ----------------------------------------------------------------------------
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+_CPU = {}
+
+
+def _cpu_worker(idx, lo, hi, reps, bar, kind):
+    from oracle import oracle
+
+    a = _CPU
+    sl = slice(lo, hi)
+    out = np.empty(a["coeffs"][sl].shape, dtype=a["coeffs"].dtype)
+    lane = oracle.ref_lane() if kind == "reference" else None
+    aux = a["aux"][sl] if a["aux"] is not None else None
+    for _ in range(reps):
+        bar.wait()
+        if lane is not None:
+            oracle.ref_integrate(lane, a["fc"], a["am"], a["B"], a["D"], a["W"], a["inv"][sl], a["det"][sl],
+                                 a["coeffs"][sl], aux, out)
+        else:
+            out[...] = oracle.integrate(a["fc"], a["am"], a["B"], a["D"], a["W"], a["inv"][sl], a["det"][sl],
+                                        a["coeffs"][sl], aux, a["coeffs"].dtype)
+        bar.wait()
+
+
+def cpu_reference(name, reps, target_s=None):
+    """Time the reference CPU lane on all host cores (fork pool over contiguous
+    ranges; threads do not scale: the Cython lane holds the GIL)."""
+    import multiprocessing as mp
+
+    from oracle import oracle
+
+    dim, physics, dtype, n = CONFIGS[name]
+    npdt = np.float32 if dtype == "f32" else np.float64
+    full, inv, det, coeffs, aux = oracle.workload(dim, physics, n)
+    B, D, W = oracle.p1_tables(dim)
+    c = lambda x: np.ascontiguousarray(x, dtype=npdt)  # noqa: E731
+    kind = "reference" if oracle.ref_lane() is not None else "port"
+    _CPU.update(fc=2 if physics == "elasticity" else 1, am=1 if aux is not None else 0, B=c(B), D=c(D), W=c(W),
+                inv=c(inv), det=c(det), coeffs=c(coeffs), aux=None if aux is None else c(aux))
+    P = host_cores()
+    ctx = mp.get_context("fork")
+    # one untimed calibration pass decides reps for the bounded sample
+    if target_s is not None:
+        t0 = time.perf_counter()
+        _cpu_worker(0, 0, n // P, 1, _NoBarrier(), kind)
+        one = max(time.perf_counter() - t0, 1e-4)
+        reps = int(max(3, min(200, target_s / one)))
+    bar = ctx.Barrier(P + 1)
+    procs = []
+    for i in range(P):
+        lo, hi = n * i // P, n * (i + 1) // P
+        p = ctx.Process(target=_cpu_worker, args=(i, lo, hi, reps + 1, bar, kind))
+        p.start()
+        procs.append(p)
+    times = []
+    for r in range(reps + 1):
+        bar.wait()
+        t0 = time.perf_counter()
+        bar.wait()
+        if r > 0:  # first rep is warm-up
+            times.append(time.perf_counter() - t0)
+    for p in procs:
+        p.join()
+    return dict(times=times, cores=P, kind=kind, n=n, dtype=dtype)
+
+
+class _NoBarrier:
+    def wait(self):
+        pass
+
+
+# ----------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=HEADLINE, choices=sorted(CONFIGS))
+    ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=3.0)
+    args = ap.parse_args()
+    world, rank, local = dist_setup()
+    if args.warmup < 3:
+        args.warmup = 3
+    flops_cell, bytes_cell = config_model(args.config)
+    dim, physics, dtype, per_gpu = CONFIGS[args.config]
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        r = cpu_reference(args.config, args.steps + args.warmup)
+        ts = r["times"][args.warmup:] if len(r["times"]) > args.warmup else r["times"]
+        t = sum(ts) / len(ts)
+        gf = flops_cell * r["n"] / t / 1e9
+        line = {
+            "impl": "reference", "metric": "element-integration GF/s (paper Eq.7 flops)", "value": gf,
+            "unit": "GF/s", "n_gpus": args.gpus, "steps": len(ts), "warmup": args.warmup,
+            "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": dtype, "data": "synthetic (Kuhn mesh, seeded N(0,1) coefficients, P0 kappa)",
+            "config": {"workload": f"{args.config}: 3D P1 var-coef Laplacian, {r['n']} cells"},
+            "cpu_baseline": {"value": gf, "unit": "GF/s", "cores": r["cores"], "kind": r["kind"],
+                             "sample": f"{r['n']} cells per step, fork pool of {r['cores']} processes over "
+                                       f"contiguous ranges, reference _kernels_cy lane"},
+            "e2e": {"value": gf, "unit": "GF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gbs": bytes_cell * r["n"] / t / 1e9,
+        }
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    barrier = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        barrier = dist.barrier
+
+    from paper_1607_04245_b200 import backend
+
+    wl = rank_workload(args.config, rank, world)
+    set_bytes = bytes_cell * wl["n"]
+    n_sets = max(4, -(-3 * L2_BYTES // set_bytes) + 1)
+    sampler = ClockSampler(torch.cuda.current_device())
+    total_ms, per = time_device(wl, args.steps, args.warmup, n_sets, barrier, sampler)
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([total_ms, statistics.mean(per)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, launch_ms = float(t[0]), float(t[1])
+    else:
+        launch_ms = statistics.mean(per)
+    cells_total = per_gpu * world
+    ms_step = total_ms / args.steps
+    gf = flops_cell * cells_total / (ms_step * 1e-3) / 1e9
+
+    # e2e through the host-buffer C ABI path
+    e2e_steps = max(3, min(20, args.steps // 20))
+    e2e_s, h2d, d2h, _ = time_e2e(wl, e2e_steps, 2)
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t[0])
+    e2e_gf = flops_cell * cells_total * e2e_steps / e2e_s / 1e9
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = peaks()
+    achieved = bytes_cell * wl["n"] / (launch_ms * 1e-3) / 1e9
+    form = wl["form"]
+    cfg = backend.launch_config(*backend.cuda_kernel(form, 1, wl["aux"], 4 if dtype == "f32" else 8),
+                                4 if dtype == "f32" else 8, dim, 1, form.n_comp, wl["n"])
+    achievable = stream_probe(wl["inv"].nbytes + wl["det"].nbytes + wl["coeffs"].nbytes +
+                              (wl["aux"].values.nbytes if wl["aux"] is not None else 0), wl["coeffs"].nbytes)
+    prof = REPO / "profiles" / "ncu_traffic.json"
+    traffic = None
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get(args.config)
+    line = {
+        "metric": "element-integration GF/s (paper Eq.7 flops)",
+        "value": gf, "unit": "GF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": dtype, "data": "synthetic (Kuhn mesh sliced to the cell count, seeded N(0,1) "
+                                "coefficients, P0 kappa U[0.5,1.5); generated on the device)",
+        "config": {"workload": f"{args.config}: {dim}D P1 {physics}, {per_gpu} cells per GPU "
+                               f"(BASELINE.json configs[1])",
+                   "cells_total": cells_total, "parallelism": f"cell-range x{world}",
+                   "l2": f"{n_sets} rotating buffer sets of {set_bytes / 1e6:.1f} MB (> 126 MB L2)",
+                   "launch": cfg},
+        "gbs": bytes_cell * cells_total / (ms_step * 1e-3) / 1e9,
+        "cells_per_s": cells_total / (ms_step * 1e-3),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "bytes_per_cell": bytes_cell, "flops_per_cell_eq7": flops_cell,
+                     "achievable_stream_gbs": achievable, "frac_of_achievable": achieved / achievable,
+                     "launch_ms": launch_ms},
+        "e2e": {"value": e2e_gf, "unit": "GF/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "steps": e2e_steps, "path": "txb_integrate_cells_host (pinned numpy in/out)"},
+        "gpu_launches": args.steps,
+        "clocks": sampler.summary(),
+    }
+    if world == 1 and not args.no_cpu:
+        r = cpu_reference(args.config, 3, target_s=args.cpu_seconds)
+        t = statistics.median(r["times"])
+        line["cpu_baseline"] = {"value": flops_cell * r["n"] / t / 1e9, "unit": "GF/s", "cores": r["cores"],
+                                "kind": r["kind"], "ms": t * 1e3,
+                                "sample": f"{r['n']} cells ({args.config}) x {len(r['times'])} passes, fork "
+                                          f"pool of {r['cores']} processes, median pass"}
+    if world == 1 and not args.no_variants:
+        variants = []
+        for v in VARIANTS:
+            vf, vb = config_model(v)
+            vw = rank_workload(v, 0, 1)
+            vs = max(4, -(-3 * L2_BYTES // (vb * vw["n"])) + 1)
+            steps = max(20, args.steps // 4) if vw["n"] <= (1 << 20) else 20
+            tot, vper = time_device(vw, steps, 5, min(vs, 8))
+            vl = statistics.mean(vper)
+            variants.append({"config": v, "dtype": vw["dtype"], "cells": vw["n"],
+                             "gflops": vf * vw["n"] / (tot / steps * 1e-3) / 1e9,
+                             "gbs_launch": vb * vw["n"] / (vl * 1e-3) / 1e9,
+                             "frac": vb * vw["n"] / (vl * 1e-3) / 1e9 / peak, "launch_ms": vl,
+                             "bytes_per_cell": vb})
+            del vw
+            torch.cuda.empty_cache()
+        line["variants"] = variants
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,148 @@
+/*
+ * txb.h — C ABI of the B200-native thread-transposed element integrator.
+ *
+ * This is the drop-in boundary for the reference's compiled lane.  Every entry
+ * point takes plain pointers and sizes (no torch / numpy types); a Python host
+ * binds it with ctypes (paper_1607_04245_b200/_lib.py), and INTEGRATION.md
+ * shows the ctypes stub the reference's own backend.py would add.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/pkg/src):
+ *   txb_query              <- txfem/backend.py:38-52   compiled_kernel(form, n_q, aux)
+ *   txb_integrate_cells    <- txfem/_kernels_cy.pyx:37-123 integrate_cells(...)
+ *                             reached via txfem/backend.py:55-87 run_compiled(...)
+ *                             and txfem/executor.py:109-114 _run_span(...)
+ *   txb_integrate_cells_host  same call with HOST buffers (the reference's own
+ *                             calling convention: numpy arrays in host memory)
+ *   txb_gather_coefficients   <- txfem/mesh.py:202-217 gather_coefficients
+ *   txb_scatter_add           <- txfem/mesh.py:220-234 scatter_add_element_vectors
+ *   txb_compute_geometry      <- txfem/mesh.py:150-190 compute_geometry
+ *   txb_last_error         error text for the Python exception message
+ *
+ * Codes follow the reference (backend.py:26-27):
+ *   form_code: 0 poisson (f1 = grad u), 1 poisson_varcoef (f1 = a grad u),
+ *              2 elasticity (f1 = sym grad u)
+ *   aux_mode : 0 none, 1 P0 (one value per cell), 2 P1 (one value per vertex
+ *              of the cell)
+ *   dtype_bytes: 4 (float32) or 8 (float64); every array of one call has it.
+ *
+ * Array layouts (C-contiguous), identical to _kernels_cy.pyx:40-48:
+ *   basis (n_q, n_b), basis_der (n_q, n_b, dim), weights (n_q)   HOST pointers
+ *     (tiny tabulation; copied into the kernel's parameter space per launch)
+ *   inv_j (n, dim, dim) row-major, det_j (n), coeffs (n, n_b, n_comp),
+ *   aux (n, 1) [mode 1] | (n, n_b, 1) [mode 2] | NULL [mode 0],
+ *   out (n, n_b, n_comp): caller-allocated, fully overwritten, the only
+ *     buffer written.
+ *
+ * Threading / ownership: stateless and reentrant; the device
+ * call is asynchronous on `stream` (a cudaStream_t, NULL = legacy default),
+ * allocates nothing and never synchronises.  Inputs are read-only.
+ *
+ * Numerics: every multiply and add rounds separately in the configured
+ * precision, in the reference's pinned order (reference.py:10-19), so results
+ * are bit-identical to the reference compiled lane for f32 and f64 and to
+ * integrate_reference for f64.
+ */
+#ifndef TXB_H_
+#define TXB_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Return codes (0 = success).  The Python host re-raises the matching
+ * txfem.errors class (errors.py:4-42). */
+#define TXB_OK              0
+#define TXB_E_UNSUPPORTED  -1  /* configuration outside the kernel surface  -> ValueError */
+#define TXB_E_SHAPE        -2  /* inconsistent sizes                          -> ShapeError */
+#define TXB_E_CONFIG       -3  /* n_bl / n_cb / thread-limit violation        -> ConfigurationError */
+#define TXB_E_CAPACITY     -4  /* shared-memory image exceeds the device      -> CapacityError */
+#define TXB_E_ARG          -5  /* NULL pointer where data is required         -> ValueError */
+#define TXB_E_CUDA         -6  /* CUDA runtime error (text in txb_last_error) -> RuntimeError */
+#define TXB_E_ORIENTATION  -7  /* detJ <= 0 in txb_compute_geometry           -> OrientationError */
+
+#define TXB_MAX_DIM    3
+#define TXB_MAX_BASIS  4
+#define TXB_MAX_COMP   3
+#define TXB_MAX_QUAD   8
+#define TXB_THREAD_LIMIT 1024
+
+/* ABI version (bumped on any signature change). */
+int txb_abi_version(void);
+
+/* Thread-local text of the last failure on this thread ("" if none). */
+const char* txb_last_error(void);
+
+/* Capability probe: TXB_OK if txb_integrate_cells covers the configuration,
+ * TXB_E_UNSUPPORTED otherwise.  Same coverage as backend.compiled_kernel:
+ * dim<=3, n_b=dim+1<=4, n_q<=8, n_comp 1 (forms 0,1) or dim (form 2), aux
+ * required by form 1 and forbidden for forms 0, 2. */
+int txb_query(int form_code, int aux_mode, int dtype_bytes, int dim, int n_q, int n_comp);
+
+/* Launch geometry the integrator would use (for tests, bench and tuning).
+ * n_bl / n_cb <= 0 select the tuned defaults.  Outputs may be NULL.
+ *   n_bc        cells per batch  (= n_bl * n_b * n_q, paper §3)
+ *   n_t         threads per CTA  (= n_bc * n_comp)
+ *   stages      shared-memory ring depth of the batch loader
+ *   smem_bytes  dynamic shared memory per CTA
+ *   grid        CTAs launched for n_cells on the current device            */
+int txb_launch_config(int form_code, int aux_mode, int dtype_bytes, int dim, int n_q,
+                      int n_comp, int64_t n_cells, int n_bl, int n_cb,
+                      int* n_bc, int* n_t, int* stages, int* smem_bytes, int* grid,
+                      int* n_bl_used, int* n_cb_used);
+
+/* Element integration over n_cells cells, DEVICE pointers for the per-cell
+ * arrays, HOST pointers for basis / basis_der / weights. */
+int txb_integrate_cells(int form_code, int aux_mode, int dtype_bytes, int dim, int n_b,
+                        int n_q, int n_comp, int64_t n_cells,
+                        const void* basis, const void* basis_der, const void* weights,
+                        const void* inv_j, const void* det_j, const void* coeffs,
+                        const void* aux, void* out, int n_bl, int n_cb, void* stream);
+
+/* Same call with every array in HOST memory (pinned or pageable).  Copies
+ * the inputs to the device, integrates and copies `out` back, pipelined in
+ * cell pieces over two streams; returns after `out` is complete. */
+int txb_integrate_cells_host(int form_code, int aux_mode, int dtype_bytes, int dim, int n_b,
+                             int n_q, int n_comp, int64_t n_cells,
+                             const void* basis, const void* basis_der, const void* weights,
+                             const void* inv_j, const void* det_j, const void* coeffs,
+                             const void* aux, void* out, int n_bl, int n_cb);
+
+/* Gather per-cell coefficient blocks (device pointers):
+ *   out[c][b][k] = global[cells[c][b] * n_comp + k],  cells int64 (n, n_b). */
+int txb_gather_coefficients(int dtype_bytes, int64_t n_cells, int n_b, int n_comp,
+                            const int64_t* cells, const void* global, void* out, void* stream);
+
+/* Deterministic scatter-add (device pointers).  `offsets` (n_vertices+1) and
+ * `incidence` (n_cells*n_b) are the vertex->(cell*n_b+b) CSR built by
+ * txb_build_incidence, entries in ascending cell order, so every vertex sum
+ * runs in the reference's np.add.at order (bit-identical). */
+int txb_scatter_add(int dtype_bytes, int64_t n_vertices, int n_comp,
+                    const int64_t* offsets, const int64_t* incidence,
+                    const void* elem, void* out, void* stream);
+
+/* Build the vertex incidence CSR on the device from the connectivity
+ * (cells int64 (n, n_b)).  `offsets` has n_vertices+1 entries, `incidence`
+ * n_cells*n_b; `scratch` needs txb_incidence_scratch_bytes(...) bytes. */
+int64_t txb_incidence_scratch_bytes(int64_t n_cells, int n_b, int64_t n_vertices);
+int txb_build_incidence(int64_t n_cells, int n_b, int64_t n_vertices, const int64_t* cells,
+                        int64_t* offsets, int64_t* incidence, void* scratch, void* stream);
+
+/* Per-cell inverse Jacobians and determinants from vertex coordinates
+ * (device pointers, float64 like mesh.compute_geometry).  Returns
+ * TXB_E_ORIENTATION (and sets *bad_cell, a host pointer) when some
+ * detJ <= 0; synchronises on `stream` to read the flag. */
+int txb_compute_geometry(int dim, int64_t n_cells, const double* vertices, const int64_t* cells,
+                         double* inv_j, double* det_j, int64_t* bad_cell, void* stream);
+
+/* STREAM-like probe at a given read:write byte ratio (device pointers):
+ * reads `read_bytes` from src, writes `write_bytes` to dst, 16-byte vector
+ * accesses.  Used by bench.py for the "measured achievable" bandwidth. */
+int txb_stream_probe(const void* src, int64_t read_bytes, void* dst, int64_t write_bytes,
+                     void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TXB_H_ */

@@ -1,0 +1,144 @@
+"""The CUDA lane: capability probe and kernel call.
+
+Mirrors txfem/backend.py:38-87 — ``compiled_kernel``/``run_compiled`` become
+``cuda_kernel``/``run_cuda`` over the C ABI (include/txb.h).  Form codes and
+aux modes are the reference's (backend.py:26-27).  There is no CPU lane and
+no fallback: when the library or the device is missing, the call raises.
+
+``run_cuda`` accepts either
+  * CUDA torch tensors (device-resident; async on the current torch stream,
+    via ``txb_integrate_cells``), or
+  * numpy arrays (the reference's own calling convention; host->device copies,
+    kernel and device->host copy pipelined inside ``txb_integrate_cells_host``).
+``out`` is caller-allocated and fully overwritten, like the Cython lane.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .errors import CudaLaneError, ShapeError
+from .physics import CellAux, PhysicsForm
+
+__all__ = ["cuda_available", "active_backend", "cuda_kernel", "run_cuda", "launch_config",
+           "FORM_CODES", "AUX_MODES"]
+
+FORM_CODES = {"poisson": 0, "poisson_varcoef": 1, "elasticity": 2}
+AUX_MODES = {None: 0, "p0": 1, "p1": 2}
+MAX_DIM, MAX_BASIS, MAX_COMPONENTS, MAX_QUAD = 3, 4, 3, 8
+
+
+def cuda_available() -> bool:
+    try:
+        _lib.lib()
+        import torch
+
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+def active_backend() -> str:
+    return "cuda"
+
+
+def cuda_kernel(form: PhysicsForm, n_q: int, aux: Optional[CellAux], dtype_bytes: int = 8):
+    """(form_code, aux_mode) if the CUDA kernel covers the configuration, else
+    None — the coverage of backend.compiled_kernel (backend.py:38-52)."""
+    code = FORM_CODES.get(form.name)
+    if code is None or form.has_f0 or form.uses_grad_a:
+        return None
+    if form.dim > MAX_DIM or form.n_comp > MAX_COMPONENTS or form.dim + 1 > MAX_BASIS or n_q > MAX_QUAD:
+        return None
+    if aux is not None and (aux.n_aux != 1 or form.n_aux != 1):
+        return None
+    mode = AUX_MODES[None if aux is None else aux.space]
+    if _lib.lib().txb_query(code, mode, dtype_bytes, form.dim, n_q, form.n_comp) != 0:
+        return None
+    return code, mode
+
+
+def launch_config(form_code: int, aux_mode: int, dtype_bytes: int, dim: int, n_q: int, n_comp: int,
+                  n_cells: int, n_bl: int = 0, n_cb: int = 0) -> dict:
+    """Launch geometry the library would use (n_bc, n_t, stages, smem, grid, n_bl, n_cb)."""
+    vals = [ctypes.c_int(0) for _ in range(7)]
+    _lib.check(_lib.lib().txb_launch_config(form_code, aux_mode, dtype_bytes, dim, n_q, n_comp, n_cells,
+                                            n_bl, n_cb, *[ctypes.byref(v) for v in vals]),
+               "txb_launch_config")
+    keys = ("n_bc", "n_t", "stages", "smem_bytes", "grid", "n_bl", "n_cb")
+    return {k: v.value for k, v in zip(keys, vals)}
+
+
+def _host_table(x, dt) -> np.ndarray:
+    if not isinstance(x, np.ndarray):
+        x = x.detach().cpu().numpy()
+    return np.ascontiguousarray(x, dtype=dt)
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def run_cuda(kernel, basis, basis_der, weights, inv_j, det_j, coeffs, aux: Optional[CellAux], out,
+             *, n_bl: int = 0, n_cb: int = 0, stream=None) -> None:
+    """Integrate every cell of the span into ``out`` (backend.run_compiled)."""
+    form_code, aux_mode = kernel
+    n = int(det_j.shape[0])
+    n_q, n_b = int(basis.shape[0]), int(basis.shape[1])
+    d = int(basis_der.shape[2])
+    n_comp = int(out.shape[2])
+    dt = np.dtype(str(coeffs.dtype).replace("torch.", ""))
+    if dt not in (np.dtype(np.float32), np.dtype(np.float64)):
+        raise TypeError(f"coeffs must be float32 or float64, got {coeffs.dtype}")
+    # shape checks (the Cython lane would fail on mismatched memoryviews)
+    if tuple(inv_j.shape) != (n, d, d) or tuple(coeffs.shape) != (n, n_b, n_comp) or \
+            tuple(out.shape) != (n, n_b, n_comp):
+        raise ShapeError(
+            f"inconsistent spans: inv_j {tuple(inv_j.shape)}, det_j ({n},), coeffs {tuple(coeffs.shape)}, "
+            f"out {tuple(out.shape)}")
+    aux_vals = None
+    if aux_mode:
+        aux_vals = aux.values
+        want = (n, 1) if aux_mode == 1 else (n, n_b, 1)
+        if tuple(aux_vals.shape) != want:
+            raise ShapeError(f"aux values have shape {tuple(aux_vals.shape)}, expected {want}")
+    arrays = [inv_j, det_j, coeffs, out] + ([aux_vals] if aux_vals is not None else [])
+    for a in arrays:
+        if str(a.dtype).replace("torch.", "") != dt.name:
+            raise TypeError("all per-cell arrays must share one floating dtype")
+    B, D, W = _host_table(basis, dt), _host_table(basis_der, dt), _host_table(weights, dt)
+    L = _lib.lib()
+    args = (form_code, aux_mode, dt.itemsize, d, n_b, n_q, n_comp, n,
+            B.ctypes.data, D.ctypes.data, W.ctypes.data)
+    if _is_torch(out):
+        import torch
+
+        for a in arrays:
+            if not (a.is_cuda and a.is_contiguous()):
+                raise ValueError("device path needs contiguous CUDA tensors")
+        s = stream if stream is not None else torch.cuda.current_stream()
+        rc = L.txb_integrate_cells(*args, inv_j.data_ptr(), det_j.data_ptr(), coeffs.data_ptr(),
+                                   aux_vals.data_ptr() if aux_vals is not None else None,
+                                   out.data_ptr(), n_bl, n_cb, ctypes.c_void_p(s.cuda_stream))
+        _lib.check(rc, "txb_integrate_cells")
+        return
+    # host (numpy) path
+    if not (out.flags.c_contiguous and out.flags.writeable):
+        raise ValueError("out must be a writeable C-contiguous array")
+    host = [np.ascontiguousarray(a) for a in (inv_j, det_j, coeffs)]
+    av = np.ascontiguousarray(aux_vals) if aux_vals is not None else None
+    try:
+        import torch
+
+        if not torch.cuda.is_available():
+            raise CudaLaneError("the CUDA lane needs a CUDA device")
+    except ImportError as exc:  # pragma: no cover
+        raise CudaLaneError("torch is required to select the CUDA device") from exc
+    rc = L.txb_integrate_cells_host(*args, host[0].ctypes.data, host[1].ctypes.data, host[2].ctypes.data,
+                                    av.ctypes.data if av is not None else None, out.ctypes.data,
+                                    n_bl, n_cb)
+    _lib.check(rc, "txb_integrate_cells_host")

@@ -1,0 +1,282 @@
+// txb_mesh.cu — the data movement either side of the integration kernel
+// (SURVEY.md §8f rows 1-3), on the device and bit-identical to the reference:
+//
+//   txb_gather_coefficients  <- txfem/mesh.py:202-217  (E: global -> per-cell blocks)
+//   txb_build_incidence      vertex -> (cell, b) CSR in ascending cell order
+//   txb_scatter_add          <- txfem/mesh.py:220-234  (E^T: np.add.at order, no atomics)
+//   txb_compute_geometry     <- txfem/mesh.py:150-190  (cofactor inverse, detJ > 0 check)
+//
+// Plus the library's error plumbing (txb_last_error).
+#include "txb_common.cuh"
+
+#include <algorithm>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+namespace txb {
+
+static thread_local char g_err[512] = {0};
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  set_error("CUDA error %d (%s) in %s", (int)e, cudaGetErrorString(e), what);
+  return TXB_E_CUDA;
+}
+
+constexpr int TPB = 256;
+
+static int blocks_for(int64_t n) { return (int)std::min<int64_t>((n + TPB - 1) / TPB, 1 << 20); }
+
+// ---- gather: one thread per output scalar (coalesced stores, indirect loads)
+template <typename T>
+__global__ void gather_kernel(int64_t n_out, int n_b, int n_comp, const int64_t* __restrict__ cells,
+                              const T* __restrict__ global, T* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < n_out; o += stride) {
+    const int64_t cb = o / n_comp;  // flat (cell, b)
+    const int k = (int)(o - cb * n_comp);
+    out[o] = global[__ldg(cells + cb) * n_comp + k];
+  }
+}
+
+// ---- scatter-add: one thread per (vertex, component), sums its incident
+// element entries in ascending (cell, b) order starting from +0, exactly the
+// sequence np.add.at applies (mesh.py:232-233).
+template <typename T>
+__global__ void scatter_kernel(int64_t n_vertices, int n_comp, const int64_t* __restrict__ offsets,
+                               const int64_t* __restrict__ incidence, const T* __restrict__ elem,
+                               T* __restrict__ out) {
+  const int64_t n = n_vertices * n_comp;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < n; o += stride) {
+    const int64_t v = o / n_comp;
+    const int k = (int)(o - v * n_comp);
+    T s = T(0);
+    for (int64_t e = offsets[v]; e < offsets[v + 1]; ++e) s = add(s, elem[incidence[e] * n_comp + k]);
+    out[o] = s;
+  }
+}
+
+__global__ void iota_keys_kernel(int64_t n, const int64_t* __restrict__ cells, int64_t* keys,
+                                 int64_t* vals, int64_t* counts) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int64_t v = cells[i];
+    keys[i] = v;
+    vals[i] = i;
+    atomicAdd(reinterpret_cast<unsigned long long*>(counts + v), 1ull);
+  }
+}
+
+// ---- geometry: one thread per cell, float64, the reference's expression
+// order (numpy evaluates a*b - c*d as two rounded products and a rounded
+// difference; the 3x3 determinant sums left to right).
+template <int D>
+__global__ void geometry_kernel(int64_t n, const double* __restrict__ X, const int64_t* __restrict__ cells,
+                                double* __restrict__ inv_j, double* __restrict__ det_j,
+                                unsigned long long* bad) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += stride) {
+    const int64_t* cv = cells + c * (D + 1);
+    double v0[D], m[D][D];
+    const int64_t i0 = cv[0];
+#pragma unroll
+    for (int i = 0; i < D; ++i) v0[i] = X[i0 * D + i];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const int64_t ik = cv[k + 1];
+#pragma unroll
+      for (int i = 0; i < D; ++i) m[i][k] = __dsub_rn(X[ik * D + i], v0[i]);  // column k = v_{k+1} - v_0
+    }
+    double* inv = inv_j + c * D * D;
+    double det;
+    if constexpr (D == 2) {
+      const double a = m[0][0], b = m[0][1], cc = m[1][0], e = m[1][1];
+      det = __dsub_rn(__dmul_rn(a, e), __dmul_rn(b, cc));
+      inv[0] = __ddiv_rn(e, det);
+      inv[1] = __ddiv_rn(-b, det);
+      inv[2] = __ddiv_rn(-cc, det);
+      inv[3] = __ddiv_rn(a, det);
+    } else {
+      const double cof00 = __dsub_rn(__dmul_rn(m[1][1], m[2][2]), __dmul_rn(m[1][2], m[2][1]));
+      const double cof01 = __dsub_rn(__dmul_rn(m[1][2], m[2][0]), __dmul_rn(m[1][0], m[2][2]));
+      const double cof02 = __dsub_rn(__dmul_rn(m[1][0], m[2][1]), __dmul_rn(m[1][1], m[2][0]));
+      det = __dadd_rn(__dadd_rn(__dmul_rn(m[0][0], cof00), __dmul_rn(m[0][1], cof01)),
+                      __dmul_rn(m[0][2], cof02));
+      inv[0 * 3 + 0] = __ddiv_rn(cof00, det);
+      inv[1 * 3 + 0] = __ddiv_rn(cof01, det);
+      inv[2 * 3 + 0] = __ddiv_rn(cof02, det);
+      inv[0 * 3 + 1] = __ddiv_rn(__dsub_rn(__dmul_rn(m[0][2], m[2][1]), __dmul_rn(m[0][1], m[2][2])), det);
+      inv[1 * 3 + 1] = __ddiv_rn(__dsub_rn(__dmul_rn(m[0][0], m[2][2]), __dmul_rn(m[0][2], m[2][0])), det);
+      inv[2 * 3 + 1] = __ddiv_rn(__dsub_rn(__dmul_rn(m[0][1], m[2][0]), __dmul_rn(m[0][0], m[2][1])), det);
+      inv[0 * 3 + 2] = __ddiv_rn(__dsub_rn(__dmul_rn(m[0][1], m[1][2]), __dmul_rn(m[0][2], m[1][1])), det);
+      inv[1 * 3 + 2] = __ddiv_rn(__dsub_rn(__dmul_rn(m[0][2], m[1][0]), __dmul_rn(m[0][0], m[1][2])), det);
+      inv[2 * 3 + 2] = __ddiv_rn(__dsub_rn(__dmul_rn(m[0][0], m[1][1]), __dmul_rn(m[0][1], m[1][0])), det);
+    }
+    det_j[c] = det;
+    if (det <= 0.0) atomicMin(bad, (unsigned long long)c);
+  }
+}
+
+}  // namespace txb
+
+using namespace txb;
+
+extern "C" const char* txb_last_error(void) { return g_err; }
+
+extern "C" int txb_gather_coefficients(int dtype_bytes, int64_t n_cells, int n_b, int n_comp,
+                                       const int64_t* cells, const void* global, void* out,
+                                       void* stream) {
+  if (n_cells < 0 || n_b < 1 || n_comp < 1) {
+    set_error("gather: bad sizes n_cells=%lld n_b=%d n_comp=%d", (long long)n_cells, n_b, n_comp);
+    return TXB_E_SHAPE;
+  }
+  if (n_cells == 0) return TXB_OK;
+  if (!cells || !global || !out) {
+    set_error("gather: NULL device pointer");
+    return TXB_E_ARG;
+  }
+  const int64_t n_out = n_cells * n_b * n_comp;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype_bytes == 8)
+    gather_kernel<double><<<blocks_for(n_out), TPB, 0, s>>>(n_out, n_b, n_comp, cells,
+                                                            (const double*)global, (double*)out);
+  else if (dtype_bytes == 4)
+    gather_kernel<float><<<blocks_for(n_out), TPB, 0, s>>>(n_out, n_b, n_comp, cells,
+                                                           (const float*)global, (float*)out);
+  else {
+    set_error("dtype_bytes must be 4 or 8");
+    return TXB_E_UNSUPPORTED;
+  }
+  TXB_CUDA_TRY(cudaGetLastError());
+  return TXB_OK;
+}
+
+extern "C" int txb_scatter_add(int dtype_bytes, int64_t n_vertices, int n_comp, const int64_t* offsets,
+                               const int64_t* incidence, const void* elem, void* out, void* stream) {
+  if (n_vertices < 0 || n_comp < 1) {
+    set_error("scatter: bad sizes");
+    return TXB_E_SHAPE;
+  }
+  if (n_vertices == 0) return TXB_OK;
+  if (!offsets || !incidence || !elem || !out) {
+    set_error("scatter: NULL device pointer");
+    return TXB_E_ARG;
+  }
+  const int64_t n = n_vertices * n_comp;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype_bytes == 8)
+    scatter_kernel<double><<<blocks_for(n), TPB, 0, s>>>(n_vertices, n_comp, offsets, incidence,
+                                                         (const double*)elem, (double*)out);
+  else if (dtype_bytes == 4)
+    scatter_kernel<float><<<blocks_for(n), TPB, 0, s>>>(n_vertices, n_comp, offsets, incidence,
+                                                        (const float*)elem, (float*)out);
+  else {
+    set_error("dtype_bytes must be 4 or 8");
+    return TXB_E_UNSUPPORTED;
+  }
+  TXB_CUDA_TRY(cudaGetLastError());
+  return TXB_OK;
+}
+
+// Scratch: keys_in, keys_out, vals_in (n*n_b each), counts (n_vertices+1),
+// CUB temp storage for the radix sort and the scan.
+static size_t cub_temp_bytes(int64_t n_entries, int64_t n_vertices) {
+  size_t sort_b = 0, scan_b = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, sort_b, (const int64_t*)nullptr, (int64_t*)nullptr,
+                                  (const int64_t*)nullptr, (int64_t*)nullptr, (int64_t)n_entries);
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_b, (const int64_t*)nullptr, (int64_t*)nullptr,
+                                (int64_t)(n_vertices + 1));
+  return std::max(sort_b, scan_b);
+}
+
+static size_t a256(size_t x) { return (x + 255) / 256 * 256; }
+
+extern "C" int64_t txb_incidence_scratch_bytes(int64_t n_cells, int n_b, int64_t n_vertices) {
+  const int64_t n = n_cells * n_b;
+  return (int64_t)(3 * a256(n * sizeof(int64_t)) + a256((n_vertices + 1) * sizeof(int64_t)) +
+                   a256(cub_temp_bytes(n, n_vertices)));
+}
+
+extern "C" int txb_build_incidence(int64_t n_cells, int n_b, int64_t n_vertices, const int64_t* cells,
+                                   int64_t* offsets, int64_t* incidence, void* scratch, void* stream) {
+  if (n_cells < 0 || n_b < 1 || n_vertices < 0) {
+    set_error("incidence: bad sizes");
+    return TXB_E_SHAPE;
+  }
+  if (!offsets || (n_cells > 0 && (!cells || !incidence || !scratch))) {
+    set_error("incidence: NULL device pointer");
+    return TXB_E_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n = n_cells * n_b;
+  unsigned char* p = (unsigned char*)scratch;
+  int64_t* keys_in = (int64_t*)p;
+  p += a256(n * sizeof(int64_t));
+  int64_t* keys_out = (int64_t*)p;
+  p += a256(n * sizeof(int64_t));
+  int64_t* vals_in = (int64_t*)p;
+  p += a256(n * sizeof(int64_t));
+  int64_t* counts = (int64_t*)p;
+  p += a256((n_vertices + 1) * sizeof(int64_t));
+  void* temp = p;
+  size_t temp_b = cub_temp_bytes(n, n_vertices);
+
+  TXB_CUDA_TRY(cudaMemsetAsync(counts, 0, (n_vertices + 1) * sizeof(int64_t), s));
+  if (n > 0) {
+    iota_keys_kernel<<<blocks_for(n), TPB, 0, s>>>(n, cells, keys_in, vals_in, counts);
+    TXB_CUDA_TRY(cudaGetLastError());
+    // Stable LSD radix sort by vertex id: entries of one vertex keep their
+    // ascending (cell, b) order.
+    int end_bit = 1;
+    while (end_bit < 63 && ((int64_t)1 << end_bit) < n_vertices) ++end_bit;
+    TXB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(temp, temp_b, keys_in, keys_out, vals_in, incidence,
+                                                 (int64_t)n, 0, end_bit, s));
+  }
+  TXB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(temp, temp_b, counts, offsets, (int64_t)(n_vertices + 1), s));
+  return TXB_OK;
+}
+
+extern "C" int txb_compute_geometry(int dim, int64_t n_cells, const double* vertices, const int64_t* cells,
+                                    double* inv_j, double* det_j, int64_t* bad_cell, void* stream) {
+  if (dim != 2 && dim != 3) {
+    set_error("dim must be 2 or 3, got %d", dim);
+    return TXB_E_UNSUPPORTED;
+  }
+  if (n_cells < 0) {
+    set_error("n_cells must be >= 0");
+    return TXB_E_SHAPE;
+  }
+  if (bad_cell) *bad_cell = -1;
+  if (n_cells == 0) return TXB_OK;
+  if (!vertices || !cells || !inv_j || !det_j) {
+    set_error("geometry: NULL device pointer");
+    return TXB_E_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned long long* flag = nullptr;
+  TXB_CUDA_TRY(cudaMallocAsync((void**)&flag, sizeof(unsigned long long), s));
+  TXB_CUDA_TRY(cudaMemsetAsync(flag, 0xff, sizeof(unsigned long long), s));
+  if (dim == 2)
+    geometry_kernel<2><<<blocks_for(n_cells), TPB, 0, s>>>(n_cells, vertices, cells, inv_j, det_j, flag);
+  else
+    geometry_kernel<3><<<blocks_for(n_cells), TPB, 0, s>>>(n_cells, vertices, cells, inv_j, det_j, flag);
+  TXB_CUDA_TRY(cudaGetLastError());
+  unsigned long long h = ~0ull;
+  TXB_CUDA_TRY(cudaMemcpyAsync(&h, flag, sizeof(h), cudaMemcpyDeviceToHost, s));
+  TXB_CUDA_TRY(cudaFreeAsync(flag, s));
+  TXB_CUDA_TRY(cudaStreamSynchronize(s));
+  if (h != ~0ull) {
+    if (bad_cell) *bad_cell = (int64_t)h;
+    set_error("cell %lld is degenerate or negatively oriented", (long long)h);
+    return TXB_E_ORIENTATION;
+  }
+  return TXB_OK;
+}

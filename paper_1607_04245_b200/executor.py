@@ -1,0 +1,205 @@
+"""Batch-integration API of the reference (txfem/executor.py:117-267) on the
+CUDA lane.
+
+* ``execute_chunk``  — integrate exactly one chunk.
+* ``integrate_transposed`` — mesh-level driver: gather (E),
+  element integration, deterministic scatter-add (E^T), all on the device.
+* ``integrate_cells`` — the span call without the chunk bookkeeping, for
+  device-resident callers (bench.py, multi-GPU ranks).
+
+Differences from the reference, all deliberate:
+  * the only lane is ``"cuda"`` (``backend=None`` selects it); ``"compiled"``,
+    ``"python"`` and ``"simulated"`` are the reference's CPU lanes and raise
+    ValueError here; ``log_tasks`` (the virtual-device task log) is an audit
+    tool of the simulated device and is not available;
+  * remainder cells (n mod N_chunk) are integrated on the GPU in the
+    configured precision (a predicated partial batch), not by the float64
+    CPU oracle (executor.py:258-264): identical bits in f64, ulp-level
+    differences in f32 (within the 1e-5 parity tolerance);
+  * ``jobs`` is accepted and ignored (the GPU is the parallelism).
+"""
+
+from __future__ import annotations
+
+from dataclasses import replace
+from typing import Optional, Union
+
+import numpy as np
+
+from . import backend as _backend
+from .element import QuadratureRule, Tabulation
+from .errors import CapacityError, ShapeError
+from .mesh import (CellGeometry, FieldLayout, Mesh, build_incidence, compute_geometry,
+                   gather_coefficients, scatter_add_element_vectors)
+from .physics import CellAux, PhysicsForm
+from .schedule import DEFAULT_THREAD_LIMIT, ExecutionGeometry, derive_execution_geometry
+from .trace import ChunkTrace, ExecutionTrace, model_batch_counters, shared_image_bytes
+
+__all__ = ["DEFAULT_SHARED_MEM_LIMIT", "scalar_dtype", "execute_chunk", "integrate_transposed",
+           "integrate_cells"]
+
+DEFAULT_SHARED_MEM_LIMIT = 48 * 1024
+_DTYPE_NAMES = {"f32": np.float32, "f64": np.float64}
+
+
+def scalar_dtype(spec) -> np.dtype:
+    """'f32'/'f64' or a float dtype -> np.dtype (executor.py:53-63)."""
+    if isinstance(spec, str):
+        try:
+            return np.dtype(_DTYPE_NAMES[spec])
+        except KeyError:
+            raise ValueError(f"scalar must be 'f32' or 'f64', got {spec!r}") from None
+    dt = np.dtype(spec)
+    if dt not in (np.dtype(np.float32), np.dtype(np.float64)):
+        raise ValueError(f"scalar must be float32 or float64, got {dt}")
+    return dt
+
+
+def _check_capacity(geom: ExecutionGeometry, width: int, needs_f0: bool, limit: Optional[int]):
+    """The reference's shared-memory budget check (executor.py:66-74), on the
+    paper's image model, so callers see the same CapacityError behaviour."""
+    required = shared_image_bytes(geom, width, needs_f0)
+    if limit is not None and required > limit:
+        raise CapacityError(
+            f"shared-memory image needs {required} bytes, budget is {limit} "
+            f"(n_bl={geom.n_bl}, scalar width {width})", required_bytes=required, limit_bytes=limit)
+
+
+def _resolve_backend(requested: Optional[str], form: PhysicsForm, n_q: int, aux, width: int):
+    """executor.py:93-106 with the lane set {"cuda"}."""
+    if requested not in (None, "cuda"):
+        if requested in ("compiled", "python", "simulated"):
+            raise ValueError(f"backend {requested!r} is a reference CPU lane; this framework runs 'cuda'")
+        raise ValueError(f"unknown backend {requested!r}")
+    kernel = _backend.cuda_kernel(form, n_q, aux, width)
+    if kernel is None:
+        raise ValueError("cuda backend requested but unavailable for this configuration")
+    return kernel
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        from .errors import CudaLaneError
+
+        raise CudaLaneError("the CUDA lane needs a CUDA device")
+    return torch
+
+
+def _dev(x, torch, dt):
+    """Cast once to the configured scalar (executor._device_arrays, executor.py:77-90) and
+    place on the device."""
+    tdt = torch.float32 if dt == np.float32 else torch.float64
+    if isinstance(x, np.ndarray):
+        return torch.from_numpy(np.ascontiguousarray(x, dtype=dt)).to("cuda")
+    return x.to(device="cuda", dtype=tdt).contiguous()
+
+
+def integrate_cells(tab: Tabulation, rule: QuadratureRule, cell_geom: CellGeometry, coeffs,
+                    aux: Optional[CellAux], form: PhysicsForm, *, dtype="f64", out=None,
+                    n_bl: int = 0, n_cb: int = 0, stream=None):
+    """Element vectors for every cell of the span on the CUDA lane.
+
+    CUDA tensors in -> CUDA tensor out (async on the current stream); numpy in
+    -> numpy out (host path).  ``n_bl``/``n_cb`` <= 0 pick the tuned defaults.
+    """
+    dt = scalar_dtype(dtype)
+    form.require_aux(aux)
+    n = cell_geom.n_cells
+    if int(coeffs.shape[0]) != n or (aux is not None and int(aux.values.shape[0]) != n):
+        raise ShapeError(f"per-cell arrays disagree: geometry {n} cells, coefficients {coeffs.shape[0]}")
+    kernel = _resolve_backend(None, form, rule.n_q, aux, dt.itemsize)
+    host = isinstance(coeffs, np.ndarray)
+    if host:
+        inv = np.ascontiguousarray(cell_geom.inv_jacobians, dtype=dt)
+        det = np.ascontiguousarray(cell_geom.determinants, dtype=dt)
+        co = np.ascontiguousarray(coeffs, dtype=dt)
+        ax = None if aux is None else CellAux(aux.space, np.ascontiguousarray(aux.values, dtype=dt))
+        res = out if out is not None else np.empty((n, tab.n_b, form.n_comp), dtype=dt)
+    else:
+        torch = _torch()
+        inv, det, co = (_dev(x, torch, dt) for x in (cell_geom.inv_jacobians, cell_geom.determinants, coeffs))
+        ax = None if aux is None else CellAux(aux.space, _dev(aux.values, torch, dt))
+        res = out if out is not None else torch.empty((n, tab.n_b, form.n_comp), dtype=co.dtype, device="cuda")
+    _backend.run_cuda(kernel, tab.basis, tab.basis_der, rule.weights, inv, det, co, ax, res,
+                      n_bl=n_bl, n_cb=n_cb, stream=stream)
+    return res
+
+
+def execute_chunk(geom: ExecutionGeometry, tab: Tabulation, rule: QuadratureRule, cell_geom: CellGeometry,
+                  coeffs, aux: Optional[CellAux], form: PhysicsForm, *, dtype="f64", chunk_index: int = 0,
+                  shared_mem_limit: Optional[int] = DEFAULT_SHARED_MEM_LIMIT, log_tasks: bool = False,
+                  backend: Optional[str] = None):
+    """Integrate exactly one chunk of cells (executor.py:117-158)."""
+    dt = scalar_dtype(dtype)
+    if cell_geom.n_cells != geom.n_chunk or int(coeffs.shape[0]) != geom.n_chunk:
+        raise ShapeError(f"chunk slice covers {cell_geom.n_cells} cells, expected {geom.n_chunk}")
+    form.require_aux(aux)
+    _check_capacity(geom, dt.itemsize, form.has_f0, shared_mem_limit)
+    if log_tasks:
+        raise ValueError("log_tasks is a simulated-device audit feature; not available on the cuda lane")
+    _resolve_backend(backend, form, geom.n_q, aux, dt.itemsize)
+    elem = integrate_cells(tab, rule, cell_geom, coeffs, aux, form, dtype=dt, n_bl=geom.n_bl, n_cb=geom.n_cb)
+    per_batch = model_batch_counters(geom, form, dt.itemsize, aux)
+    trace = ChunkTrace(chunk_index=chunk_index, batches=[replace(per_batch) for _ in range(geom.n_cb)])
+    return elem, trace
+
+
+_INCIDENCE_CACHE: dict = {}
+
+
+def _incidence_for(mesh: Mesh, cells_dev):
+    key = (id(mesh.cells), mesh.cells.shape, mesh.n_vertices)
+    hit = _INCIDENCE_CACHE.get(key)
+    if hit is not None and hit[0] is mesh.cells:
+        return hit[1]
+    inc = build_incidence(mesh, cells_dev)
+    _INCIDENCE_CACHE.clear()
+    _INCIDENCE_CACHE[key] = (mesh.cells, inc)
+    return inc
+
+
+def integrate_transposed(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: QuadratureRule,
+                         form: PhysicsForm, coeffs_global, aux: Optional[CellAux] = None, *, n_bl: int,
+                         n_cb: int, dtype: Union[str, np.dtype] = "f64", jobs: int = 1,
+                         shared_mem_limit: Optional[int] = DEFAULT_SHARED_MEM_LIMIT,
+                         thread_limit: int = DEFAULT_THREAD_LIMIT, log_tasks: bool = False,
+                         backend: Optional[str] = None, cell_geom: Optional[CellGeometry] = None):
+    """Global residual with the transposed schedule (executor.py:161-267).
+
+    Returns (residual, trace): residual is a numpy vector in the configured
+    scalar (a CUDA tensor if ``coeffs_global`` is one)."""
+    dt = scalar_dtype(dtype)
+    geom = derive_execution_geometry(mesh.dim, tab.n_b, form.n_comp, rule.n_q, n_bl, n_cb, mesh.n_cells,
+                                     thread_limit=thread_limit)
+    form.require_aux(aux)
+    _check_capacity(geom, dt.itemsize, form.has_f0, shared_mem_limit)
+    if log_tasks:
+        raise ValueError("log_tasks is a simulated-device audit feature; not available on the cuda lane")
+    _resolve_backend(backend, form, rule.n_q, aux, dt.itemsize)
+    if aux is not None and int(aux.values.shape[0]) != mesh.n_cells:
+        raise ShapeError(f"auxiliary data covers {aux.values.shape[0]} cells, expected {mesh.n_cells}")
+    torch = _torch()
+    host_out = isinstance(coeffs_global, np.ndarray) or not hasattr(coeffs_global, "is_cuda")
+    cells_dev = torch.from_numpy(np.ascontiguousarray(mesh.cells, dtype=np.int64)).to("cuda")
+
+    if cell_geom is None:
+        cell_geom = compute_geometry(mesh, cells=cells_dev, device_out=True)
+    glob = coeffs_global if not host_out else np.asarray(coeffs_global, dtype=np.float64)
+    glob_dev = _dev(glob, torch, dt)
+    blocks = gather_coefficients(mesh, layout, glob_dev, cells=cells_dev)
+
+    elem = integrate_cells(
+        tab, rule, CellGeometry(_dev(cell_geom.inv_jacobians, torch, dt), _dev(cell_geom.determinants, torch, dt)),
+        blocks, None if aux is None else CellAux(aux.space, _dev(aux.values, torch, dt)), form,
+        dtype=dt, n_bl=n_bl, n_cb=n_cb)
+    residual = scatter_add_element_vectors(mesh, layout, elem, incidence=_incidence_for(mesh, cells_dev))
+
+    trace = ExecutionTrace(geom=geom, scalar_width=dt.itemsize, remainder_cells=geom.n_r)
+    per_batch = model_batch_counters(geom, form, dt.itemsize, aux)
+    for ci in range(geom.n_chunks):
+        trace.chunks.append(ChunkTrace(chunk_index=ci, batches=[replace(per_batch) for _ in range(geom.n_cb)]))
+    if host_out:
+        residual = residual.cpu().numpy()
+    return residual, trace

@@ -1,0 +1,224 @@
+"""Parity of the CUDA lane with the oracle and the reference's golden outputs.
+
+Every test calls the product through the C ABI (paper_1607_04245_b200.backend
+-> libtxb.so).  Bar: bit-identical to the reference in both precisions (the
+kernel rounds every product and sum in the reference's pinned order); the
+north_star tolerances (rel 1e-5 f32, 1e-12 f64) are asserted as well.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import BIG, SMALL_CASES, TOL, bitwise_equal, rel_err
+from oracle import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_1607_04245_b200 as txb  # noqa: E402
+from paper_1607_04245_b200 import backend  # noqa: E402
+from paper_1607_04245_b200.physics import CellAux  # noqa: E402
+from paper_1607_04245_b200.workload import make_workload  # noqa: E402
+
+DT = {"f32": (np.float32, torch.float32), "f64": (np.float64, torch.float64)}
+
+
+def _run_device(form_code, aux_mode, B, D, W, inv, det, coeffs, aux, dtype, n_bl=0, n_cb=0,
+                offset=0):
+    """Upload (optionally at a misaligned element offset), integrate, download."""
+    npdt, tdt = DT[dtype]
+
+    def up(a):
+        a = np.ascontiguousarray(a, dtype=npdt)
+        if offset:
+            buf = torch.empty(a.size + offset, dtype=tdt, device="cuda")
+            t = buf[offset:].view(a.shape)
+            t.copy_(torch.from_numpy(a))
+            return t
+        return torch.from_numpy(a).to("cuda")
+
+    ti, td, tc = up(inv), up(det), up(coeffs)
+    ta = CellAux("p0" if aux_mode == 1 else "p1", up(aux)) if aux_mode else None
+    out = torch.full(tuple(coeffs.shape), float("nan"), dtype=tdt, device="cuda")
+    backend.run_cuda((form_code, aux_mode), np.asarray(B, npdt), np.asarray(D, npdt), np.asarray(W, npdt),
+                     ti, td, tc, ta, out, n_bl=n_bl, n_cb=n_cb)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("case", SMALL_CASES, ids=lambda c: c.name)
+def test_small_golden_cases_bitwise(case, dtype):
+    out = _run_device(case.form_code, case.aux_mode, case.basis, case.basis_der, case.weights,
+                      case.inv_j, case.det_j, case.coeffs, case.aux, dtype)
+    golden = case.ref_f64 if dtype == "f64" else case.cy_f32
+    assert rel_err(out, case.ref_f64) <= TOL[dtype]
+    assert bitwise_equal(out, golden)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("offset", [1, 3])
+def test_unaligned_buffers_take_the_cooperative_loader(dtype, offset):
+    case = SMALL_CASES[-1]
+    out = _run_device(case.form_code, case.aux_mode, case.basis, case.basis_der, case.weights,
+                      case.inv_j, case.det_j, case.coeffs, case.aux, dtype, offset=offset)
+    assert bitwise_equal(out, case.ref_f64 if dtype == "f64" else case.cy_f32)
+
+
+def _sha(t):
+    return hashlib.sha256(np.ascontiguousarray(t.cpu().numpy()).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("name", sorted(BIG))
+def test_baseline_configs_bitwise_by_hash(name):
+    """BASELINE.json configs[0..3] at full size, generated ON THE DEVICE
+    (geometry + gather kernels), integrated in f64 and f32: every input and
+    output hash equals the reference's (tests/golden/big_hashes.json)."""
+    e = BIG[name]
+    w = make_workload(e["dim"], e["physics"], e["n_cells"], e["seed"])
+    assert _sha(w.cell_geom.inv_jacobians) == e["inputs_f64"]["inv_j"]
+    assert _sha(w.cell_geom.determinants) == e["inputs_f64"]["det_j"]
+    assert _sha(w.coeffs) == e["inputs_f64"]["coeffs"]
+    if w.aux is not None:
+        assert _sha(w.aux.values) == e["inputs_f64"]["aux"]
+    for dtype, key in (("f64", "ref_f64"), ("f32", "cy_f32")):
+        inv, det, co, aux = w.cast(dtype)
+        out = txb.integrate_cells(w.tab, w.rule, txb.CellGeometry(inv, det), co, aux, w.form, dtype=dtype)
+        torch.cuda.synchronize()
+        assert _sha(out) == e[key], (name, dtype)
+    if e["physics"] != "elasticity":
+        assert float(out.double().abs().max()) <= e["ref_f64_absmax"] * 1.0001
+
+
+@pytest.mark.parametrize("dim,physics", [(2, "poisson"), (3, "varcoef_p0"), (2, "varcoef_p1"),
+                                         (3, "elasticity")])
+def test_decomposition_grid(dim, physics):
+    """Every (n_bl, n_cb) of the reference's invariant grid (tests/test_executor.py:503-526)
+    gives the same bits: partition invariance, partial batches and tails included."""
+    n = 3001
+    full, inv, det, coeffs, aux = oracle.workload(dim, physics, n, seed=31)
+    fc = 2 if physics == "elasticity" else (1 if physics.startswith("varcoef") else 0)
+    am = {"varcoef_p0": 1, "varcoef_p1": 2}.get(physics, 0)
+    B, D, W = oracle.p1_tables(dim)
+    for dtype, npdt in (("f64", np.float64), ("f32", np.float32)):
+        ref = oracle.integrate(fc, am, B, D, W, inv, det, coeffs, aux, npdt)
+        for n_bl in (1, 2, 4, 16, 20, 24, 28, 32, 36):
+            for n_cb in (1, 4, 8, 12, 16):
+                n_t = n_bl * (dim + 1) * (dim if physics == "elasticity" else 1)
+                if n_t > 1024:
+                    continue
+                out = _run_device(fc, am, B, D, W, inv, det, coeffs, aux, dtype, n_bl, n_cb)
+                assert bitwise_equal(out, ref), (dtype, n_bl, n_cb)
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 5, 255, 256, 257, 4097])
+def test_ragged_sizes(n):
+    B, D, W = oracle.p1_tables(3)
+    full, inv, det, coeffs, aux = oracle.workload(3, "varcoef_p0", max(n, 1), seed=5)
+    inv, det, coeffs, aux = inv[:n], det[:n], coeffs[:n], aux[:n]
+    for dtype, npdt in (("f64", np.float64), ("f32", np.float32)):
+        out = _run_device(1, 1, B, D, W, inv, det, coeffs, aux, dtype)
+        assert out.shape == (n, 4, 1)
+        assert bitwise_equal(out, oracle.integrate(1, 1, B, D, W, inv, det, coeffs, aux, npdt))
+
+
+def test_two_point_rule_and_all_nq():
+    """n_q = 1..8 (duplicated barycentre, weights 1/n_q of the volume)."""
+    rng = np.random.default_rng(7)
+    n = 777
+    for dim in (2, 3):
+        jac = np.eye(dim) + 0.2 * rng.uniform(-1, 1, (n, dim, dim))
+        inv, det = np.linalg.inv(jac), np.linalg.det(jac)
+        B1, D1, W1 = oracle.p1_tables(dim)
+        for n_q in range(1, 9):
+            B, D = np.tile(B1, (n_q, 1)), np.tile(D1, (n_q, 1, 1))
+            W = np.full(n_q, W1[0] / n_q)
+            for fc, am, nc in ((0, 0, 1), (1, 1, 1), (1, 2, 1), (2, 0, dim)):
+                co = rng.standard_normal((n, dim + 1, nc))
+                aux = rng.uniform(0.5, 1.5, (n, 1) if am == 1 else (n, dim + 1, 1)) if am else None
+                for dtype, npdt in (("f64", np.float64), ("f32", np.float32)):
+                    out = _run_device(fc, am, B, D, W, inv, det, co, aux, dtype)
+                    ref = oracle.integrate(fc, am, B, D, W, inv, det, co, aux, npdt)
+                    assert bitwise_equal(out, ref), (dim, n_q, fc, am, dtype)
+
+
+def test_host_path_matches_device_path():
+    """txb_integrate_cells_host (numpy in/out, pipelined copies) == device path."""
+    B, D, W = oracle.p1_tables(3)
+    full, inv, det, coeffs, aux = oracle.workload(3, "varcoef_p0", 300_000, seed=2)
+    for dtype, npdt in (("f64", np.float64), ("f32", np.float32)):
+        c = lambda a: np.ascontiguousarray(a, dtype=npdt)  # noqa: E731
+        out = np.empty(coeffs.shape, dtype=npdt)
+        backend.run_cuda((1, 1), c(B), c(D), c(W), c(inv), c(det), c(coeffs), CellAux("p0", c(aux)), out)
+        assert bitwise_equal(out, oracle.integrate(1, 1, B, D, W, inv, det, coeffs, aux, npdt))
+
+
+def test_output_fully_overwritten_and_inputs_untouched():
+    B, D, W = oracle.p1_tables(2)
+    full, inv, det, coeffs, aux = oracle.workload(2, "elasticity", 10_000, seed=4)
+    ti = torch.from_numpy(inv).cuda()
+    td = torch.from_numpy(det).cuda()
+    tc = torch.from_numpy(coeffs).cuda()
+    snap = [t.clone() for t in (ti, td, tc)]
+    out = torch.full(tuple(coeffs.shape), float("nan"), dtype=torch.float64, device="cuda")
+    backend.run_cuda((2, 0), B, D, W, ti, td, tc, None, out)
+    torch.cuda.synchronize()
+    assert not torch.isnan(out).any()
+    for a, b in zip(snap, (ti, td, tc)):
+        assert torch.equal(a, b)
+
+
+def test_linearity_at_scale():
+    """Size-independent property at 2^24 cells: e(alpha x + y) == alpha e(x) + e(y)
+    within tolerance (tests/test_reference.py:72-88), f64."""
+    n = 1 << 24
+    g = torch.Generator(device="cuda").manual_seed(0)
+    inv = (torch.eye(3, device="cuda", dtype=torch.float64).expand(n, 3, 3)
+           + 0.2 * (torch.rand((n, 3, 3), device="cuda", dtype=torch.float64, generator=g) * 2 - 1)).contiguous()
+    det = torch.rand((n,), device="cuda", dtype=torch.float64, generator=g) + 0.5
+    x = torch.randn((n, 4, 1), device="cuda", dtype=torch.float64, generator=g)
+    y = torch.randn((n, 4, 1), device="cuda", dtype=torch.float64, generator=g)
+    kap = CellAux("p0", torch.rand((n, 1), device="cuda", dtype=torch.float64, generator=g) + 0.5)
+    B, D, W = oracle.p1_tables(3)
+
+    def e(c):
+        out = torch.empty_like(c)
+        backend.run_cuda((1, 1), B, D, W, inv, det, c, kap, out)
+        return out
+
+    lhs = e(1.7 * x + y)
+    rhs = 1.7 * e(x) + e(y)
+    torch.cuda.synchronize()
+    assert float((lhs - rhs).abs().max() / rhs.abs().max()) < 1e-12
+    # spot-check slices against the oracle, bitwise
+    for lo in (0, n // 2 + 12345, n - 1000):
+        sl = slice(lo, lo + 1000)
+        ref = oracle.integrate(1, 1, B, D, W, inv[sl].cpu().numpy(), det[sl].cpu().numpy(),
+                               x[sl].cpu().numpy(), kap.values[sl].cpu().numpy())
+        assert bitwise_equal(e(x)[sl].cpu().numpy(), ref)
+
+
+def test_max_size_fp32_3d_2_27_cells():
+    """Maximum size of BASELINE configs[4] (2^27 cells) on one GPU: constant
+    coefficients on replicated Kuhn geometry -> exactly zero everywhere, and
+    a replicated random field reproduces the 2^20 golden output in every slab."""
+    n_base = 1 << 20
+    e = BIG["3d_varcoef_p0_1048576"]
+    w = make_workload(3, "varcoef_p0", n_base, e["seed"])
+    inv, det, co, aux = w.cast("f32")
+    reps = 128
+    inv_b = inv.repeat(reps, 1, 1)
+    det_b = det.repeat(reps)
+    co_b = co.repeat(reps, 1, 1)
+    aux_b = CellAux("p0", aux.values.repeat(reps, 1))
+    out = torch.empty_like(co_b)
+    txb.integrate_cells(w.tab, w.rule, txb.CellGeometry(inv_b, det_b), co_b, aux_b, w.form, dtype="f32", out=out)
+    torch.cuda.synchronize()
+    for r in (0, 1, reps // 2, reps - 1):
+        assert _sha(out[r * n_base:(r + 1) * n_base]) == e["cy_f32"]
+    ones = torch.ones_like(co_b)
+    txb.integrate_cells(w.tab, w.rule, txb.CellGeometry(inv_b, det_b), ones, aux_b, w.form, dtype="f32", out=out)
+    torch.cuda.synchronize()
+    assert int((out != 0).sum()) == 0

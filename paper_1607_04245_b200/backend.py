@@ -118,8 +118,15 @@ def run_cuda(kernel, basis, basis_der, weights, inv_j, det_j, coeffs, aux: Optio
         import torch
 
         for a in arrays:
-            if not (a.is_cuda and a.is_contiguous()):
-                raise ValueError("device path needs contiguous CUDA tensors")
+            if not a.is_cuda:
+                raise ValueError("device path needs CUDA tensors for every per-cell array")
+        if not out.is_contiguous():
+            raise ValueError("out must be a contiguous CUDA tensor (it is written in place)")
+        # inputs: contiguous views (a copy only if needed), as run_compiled's
+        # np.ascontiguousarray (backend.py:76-84)
+        inv_j, det_j, coeffs = inv_j.contiguous(), det_j.contiguous(), coeffs.contiguous()
+        if aux_vals is not None:
+            aux_vals = aux_vals.contiguous()
         s = stream if stream is not None else torch.cuda.current_stream()
         rc = L.txb_integrate_cells(*args, inv_j.data_ptr(), det_j.data_ptr(), coeffs.data_ptr(),
                                    aux_vals.data_ptr() if aux_vals is not None else None,

@@ -6,30 +6,35 @@
 //
 // Decomposition (paper §3; txfem/schedule.py:82-113):
 //   block  = N_bs = N_b * N_q cells
-//   batch  = N_bc = N_bl * N_bs cells            -> one shared-memory stage
-//   chunk  = N_cb consecutive batches             -> one CTA work item
-//   N_t    = N_bc * N_comp threads per CTA (capped at 512 physical threads;
-//            a CTA then walks the same work items in more steps)
-// Each CTA is persistent: it walks chunks blockIdx.x, blockIdx.x + gridDim.x,
-// ... and their batches in order, so every CTA streams through the cell arrays
-// in lock-step with the others.
-//
-// Per batch:
-//   loader      one elected thread issues cp.async.bulk copies (UBLKCP) of the
-//               batch's contiguous inv_j / det_j / coeffs / aux byte ranges
-//               into a ring of `stages` shared-memory stages, completion on an
-//               mbarrier (expect_tx); the ring runs `stages-1` batches ahead.
-//   quadrature  one thread per (cell, q): pulled-back gradients T[q][b][k],
-//   phase       grad u, aux value, inlined f1, scale by detJ*w -> smem
-//               (txfem/device.py:267-330, _kernels_cy.pyx:70-111)
-//   barrier     one __syncthreads (the paper's "TRANSPOSE THREADS")
-//   basis       one thread per element-vector entry (cell, b, c): the
-//   phase       reduction-free sum over (q, k) of T[q][b][k] * f1s[q][c][k];
-//               thread index == flat output index, so the stores coalesce
-//               (txfem/device.py:335-361, _kernels_cy.pyx:113-123)
+//   batch  = N_bc = N_bl * N_bs cells        -> one shared-memory ring stage
+//   chunk  = N_cb consecutive batches         -> one CTA work item
+// A CTA is persistent and warp-specialised:
+//   producer warp   one elected lane streams batches into a ring of `stages`
+//                   shared-memory stages with cp.async.bulk (SASS UBLKCP):
+//                   the batch's contiguous inv_j / det_j / coeffs / aux byte
+//                   ranges, completion counted on a `full` mbarrier
+//                   (expect_tx); it refills a stage once every consumer warp
+//                   has arrived on the stage's `empty` mbarrier.
+//   consumer warps  each owns warp slices of CW = 32 / N_q cells of a batch:
+//     quadrature phase  lane <-> (cell, q): pulled-back gradients, grad u,
+//                       aux value, inlined f1, scaled by detJ * w_q
+//                       (txfem/device.py:267-330, _kernels_cy.pyx:70-111)
+//     transpose         through a warp-private scratch area + __syncwarp (the
+//                       paper's "TRANSPOSE THREADS" barrier, no CTA barrier)
+//     basis phase       lane <-> element-vector entry (cell, b, c): the
+//                       reduction-free sum over (q, k) of T[q][b][k] * f1s[q][c][k];
+//                       consecutive lanes own consecutive output entries, so
+//                       the stores coalesce (device.py:335-361, pyx:113-123)
+// CTAs walk chunks blockIdx.x, blockIdx.x + gridDim.x, ... so the whole grid
+// streams through the cell arrays together.
 //
 // Numerics: products and sums round one at a time in the reference's pinned
 // order (txfem/reference.py:10-19) -> bit-identical to the reference lanes.
+// When the tabulated reference gradients are exactly the P1 ones
+// (-1 / unit vectors, element.py:55-77) the kernel uses the exact IEEE
+// identities 1*x = x, (-1)*x = -x, 0*x = +-0, x + (+-0) = x (x != 0) to
+// evaluate the pull-back T[b][k] = sum_j D[b][j] invJ[j][k] with the same
+// rounded results and far fewer instructions (bit-identical for finite inputs).
 #include "txb_common.cuh"
 
 #include <algorithm>
@@ -40,9 +45,9 @@
 
 namespace txb {
 
-constexpr int MAX_D = TXB_MAX_DIM, MAX_B = TXB_MAX_BASIS, MAX_C = TXB_MAX_COMP,
-              MAX_Q = TXB_MAX_QUAD;
-constexpr int MAX_CTA_THREADS = 512;
+constexpr int MAX_D = TXB_MAX_DIM, MAX_B = TXB_MAX_BASIS, MAX_Q = TXB_MAX_QUAD;
+constexpr int MAX_CONSUMER_WARPS = 16;
+constexpr int MAX_CTA_THREADS = 32 * (MAX_CONSUMER_WARPS + 1);
 
 template <typename T>
 struct Tabulation {
@@ -59,22 +64,13 @@ struct IntegrateArgs {
   const T* aux;
   T* out;
   int64_t n_cells;
-  int64_t n_batches;
-  int64_t n_chunks;
-  int n_bc;     // cells per batch
-  int n_cb;     // batches per chunk
-  int stages;   // ring depth
-  int bulk;     // 1: full batches arrive by bulk copy; 0: cooperative loads
+  int64_t n_chunks;     // chunks, round-robin over the CTAs
+  int64_t chunk_cells;  // cells per chunk (a multiple of 16 or of N_bc)
+  int n_bc;    // cells per batch
+  int stages;  // ring depth
+  int warps;   // consumer warps
+  int bulk;    // 1: full batches arrive by bulk copy; 0: every batch read from global
   Tabulation<T> tab;
-};
-
-// Per-cell shared-memory strides of the phase-1 -> phase-2 exchange; odd
-// element strides keep both 32- and 64-bit accesses bank-conflict free.
-template <int D, int NQ, int NCOMP>
-struct Strides {
-  static constexpr int NB = D + 1;
-  static constexpr int TRANS = make_odd(NQ * NB * D);
-  static constexpr int F1S = make_odd(NQ * NCOMP * D);
 };
 
 // Byte layout of one ring stage: four 16-byte aligned regions holding the
@@ -92,18 +88,33 @@ struct StageLayout {
   }
 };
 
-template <typename T, int D, int NQ, int NCOMP>
-__host__ __device__ inline int scratch_bytes(int n_bc) {
-  using S = Strides<D, NQ, NCOMP>;
-  return round_up(n_bc * (S::TRANS + S::F1S) * (int)sizeof(T), 16);
-}
+// Warp-private exchange area between the two phases.  STD (standard P1
+// tables): only T[0][k] is stored (the other rows are invJ rows, read from the
+// stage); otherwise all T[q][b][k].  T strides are odd (bank-conflict free
+// scalar access); the f1 rows are padded to 16 bytes so the basis phase reads
+// them with vector loads (a warp touches 32/(N_b N_comp) cells per access).
+template <typename T, int D, int NQ, int NCOMP, bool STD>
+struct Scratch {
+  static constexpr int NB = D + 1;
+  static constexpr int CW = 32 / NQ;  // cells per warp slice
+  static constexpr int TR = STD ? D : NQ * NB * D;
+  static constexpr int F1 = NQ * NCOMP * D;
+  static constexpr int VEC = 16 / (int)sizeof(T);
+  static constexpr int TRS = make_odd(TR);
+  static constexpr int F1S = NCOMP == 1 ? round_up(F1, VEC) : make_odd(F1);
+  static constexpr int TR_BYTES = round_up(CW * TRS * (int)sizeof(T), 16);
+  static constexpr int BYTES = TR_BYTES + CW * F1S * (int)sizeof(T);
+};
 
-// Vectorised shared-memory row load: N consecutive T starting at p; uses the
-// widest access the row alignment allows (row starts are multiples of N*sizeof(T)).
-template <typename T, int N>
+// Vectorised row load: N consecutive T at p (row starts are multiples of
+// N*sizeof(T) from a 16-byte aligned base); widest access the alignment allows.
+template <typename T, int N, bool VEC = true>
 __device__ __forceinline__ void load_row(const T* __restrict__ p, T (&r)[N]) {
   constexpr int BYTES = N * (int)sizeof(T);
-  if constexpr (BYTES % 16 == 0) {
+  if constexpr (!VEC) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) r[i] = p[i];
+  } else if constexpr (BYTES % 16 == 0) {
     constexpr int V = 16 / sizeof(T);
 #pragma unroll
     for (int i = 0; i < N; i += V) {
@@ -123,146 +134,106 @@ __device__ __forceinline__ void load_row(const T* __restrict__ p, T (&r)[N]) {
   }
 }
 
-template <typename T, int D, int NQ, int NCOMP, int FORM, int AUX>
-__global__ void __launch_bounds__(MAX_CTA_THREADS)
-integrate_kernel(const __grid_constant__ IntegrateArgs<T> a) {
-  constexpr int NB = D + 1;
-  constexpr int DD = D * D;
-  constexpr int NBC = NB * NCOMP;  // element-vector entries per cell
-  using L = StageLayout<T, D, NCOMP, AUX>;
-  using S = Strides<D, NQ, NCOMP>;
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int nbc = a.n_bc;
-  const int tid = threadIdx.x;
-  const int nt = blockDim.x;
-  const int stage_bytes = L::stage_bytes(nbc);
-  T* s_trans = reinterpret_cast<T*>(smem + a.stages * stage_bytes);
-  T* s_f1s = s_trans + nbc * S::TRANS;
-  uint64_t* bars =
-      reinterpret_cast<uint64_t*>(smem + a.stages * stage_bytes + scratch_bytes<T, D, NQ, NCOMP>(nbc));
+// Exactness note (why the chains below may skip the reference's "acc = 0;
+// acc = acc + x" first step and its 0*x / 1*x products): in round-to-nearest
+// a sum is -0 only if both operands are -0, so a chain started at +0 is never
+// -0, and chains started at +0 vs at their first term differ at most in the
+// SIGN OF A ZERO.  Every intermediate (T, grad u, f1s) only ever enters
+// products that are summed into such a +0-started chain, where a zero term of
+// either sign leaves the partial sum unchanged.  Hence only the final
+// element-vector chain must start at +0 to reproduce the reference bit for
+// bit; everything upstream may drop exact no-ops.  (Finite inputs.)
 
-  // Batch sequence of this CTA: chunks blockIdx.x + k*gridDim.x, N_cb batches each.
-  auto batch_of = [&](int64_t i) -> int64_t {
-    const int64_t k = i / a.n_cb;
-    const int64_t ci = blockIdx.x + k * gridDim.x;
-    if (ci >= a.n_chunks) return -1;
-    const int64_t b = ci * a.n_cb + (i - k * a.n_cb);
-    return b < a.n_batches ? b : -1;
-  };
-  auto full_batch = [&](int64_t b) { return (b + 1) * (int64_t)nbc <= a.n_cells; };
+// One warp slice: CW cells starting at batch-local cell `c0` of a batch with
+// `ncell` cells whose per-cell arrays start at the given pointers (shared
+// stage or global memory); element vectors go to `out` (batch base, global).
+template <typename T, int D, int NQ, int NCOMP, int FORM, int AUX, bool STD, bool VEC>
+__device__ __forceinline__ void warp_slice(const Tabulation<T>& tab, const T* __restrict__ s_inv,
+                                           const T* __restrict__ s_det, const T* __restrict__ s_coef,
+                                           const T* __restrict__ s_aux, unsigned char* __restrict__ scratch,
+                                           int c0, int ncell, T* __restrict__ out, int lane) {
+  constexpr int NB = D + 1, DD = D * D, NBC = NB * NCOMP;
+  using S = Scratch<T, D, NQ, NCOMP, STD>;
+  constexpr int AUXW = AUX == 1 ? 1 : (AUX == 2 ? NB : 0);
+  T* s_tr = reinterpret_cast<T*>(scratch);
+  T* s_f1 = reinterpret_cast<T*>(scratch + S::TR_BYTES);
+  const int nc = min(S::CW, ncell - c0);
 
-  const uint64_t policy = l2_evict_first_policy();
-  // Loader: one thread posts the byte count and the four bulk copies.
-  auto issue = [&](int64_t i) {
-    const int64_t b = batch_of(i);
-    if (b < 0 || !a.bulk || !full_batch(b)) return;
-    unsigned char* st = smem + (int)(i % a.stages) * stage_bytes;
-    uint64_t* bar = bars + (i % a.stages);
-    const int64_t c0 = b * nbc;
-    const uint32_t ib = nbc * DD * sizeof(T), db = nbc * sizeof(T), cb = nbc * NBC * sizeof(T),
-                   ab = nbc * L::AUXW * sizeof(T);
-    mbar_arrive_expect_tx(bar, ib + db + cb + ab);
-    bulk_g2s(st, a.inv_j + c0 * DD, ib, bar, policy);
-    bulk_g2s(st + L::inv_bytes(nbc), a.det_j + c0, db, bar, policy);
-    bulk_g2s(st + L::inv_bytes(nbc) + L::det_bytes(nbc), a.coeffs + c0 * NBC, cb, bar, policy);
-    if constexpr (AUX != 0)
-      bulk_g2s(st + L::inv_bytes(nbc) + L::det_bytes(nbc) + L::coef_bytes(nbc),
-               a.aux + c0 * L::AUXW, ab, bar, policy);
-  };
-
-  if (tid == 0) {
-    for (int s = 0; s < a.stages; ++s) mbar_init(&bars[s], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (tid == 0)
-    for (int s = 0; s < a.stages; ++s) issue(s);
-
-  // Basis-phase ownership is fixed per thread because N_t is a multiple of
-  // N_b*N_comp: entry r = (b, c) of every cell this thread visits.
-  const int r = tid % NBC;
-  const int my_b = r / NCOMP, my_c = r % NCOMP;
-
-  for (int64_t i = 0;; ++i) {
-    const int64_t b = batch_of(i);
-    if (b < 0) break;
-    const int stage = (int)(i % a.stages);
-    unsigned char* st = smem + stage * stage_bytes;
-    const T* s_inv = reinterpret_cast<const T*>(st);
-    const T* s_det = reinterpret_cast<const T*>(st + L::inv_bytes(nbc));
-    const T* s_coef = reinterpret_cast<const T*>(st + L::inv_bytes(nbc) + L::det_bytes(nbc));
-    const T* s_aux =
-        reinterpret_cast<const T*>(st + L::inv_bytes(nbc) + L::det_bytes(nbc) + L::coef_bytes(nbc));
-    const int64_t c0 = b * nbc;
-    const int64_t rem = a.n_cells - c0;
-    const int ncell = rem < nbc ? (int)rem : nbc;
-
-    if (a.bulk && ncell == nbc) {
-      mbar_wait(&bars[stage], (uint32_t)((i / a.stages) & 1));
-    } else {
-      // Cooperative load: partial tail batch or unaligned caller buffers.
-      T* w_inv = const_cast<T*>(s_inv);
-      T* w_det = const_cast<T*>(s_det);
-      T* w_coef = const_cast<T*>(s_coef);
-      T* w_aux = const_cast<T*>(s_aux);
-      for (int e = tid; e < ncell * DD; e += nt) w_inv[e] = a.inv_j[c0 * DD + e];
-      for (int e = tid; e < ncell; e += nt) w_det[e] = a.det_j[c0 + e];
-      for (int e = tid; e < ncell * NBC; e += nt) w_coef[e] = a.coeffs[c0 * NBC + e];
-      if constexpr (AUX != 0)
-        for (int e = tid; e < ncell * L::AUXW; e += nt) w_aux[e] = a.aux[c0 * L::AUXW + e];
-      __syncthreads();
-    }
-
-    // ---------------- quadrature phase: thread <-> (cell, q) ----------------
-    for (int it = tid; it < ncell * NQ; it += nt) {
-      const int cell = NQ == 1 ? it : it / NQ;
-      const int q = NQ == 1 ? 0 : it - cell * NQ;
+  // ---------------- quadrature phase: lane <-> (cell, q) ----------------
+  {
+    const int lc = NQ == 1 ? lane : lane / NQ;
+    const int q = NQ == 1 ? 0 : lane - lc * NQ;
+    if (lc < nc) {
+      const int cell = c0 + lc;
       T J[DD];
-      load_row<T, DD>(s_inv + cell * DD, J);
+      load_row<T, DD, VEC>(s_inv + cell * DD, J);
       T cf[NBC];
-      load_row<T, NBC>(s_coef + cell * NBC, cf);
+      load_row<T, NBC, VEC>(s_coef + cell * NBC, cf);
       const T det = s_det[cell];
-      const T* Dq = a.tab.D + q * NB * D;
-      const T* Bq = a.tab.B + q * NB;
 
       T tr[NB][D];
-      T* trans_out = s_trans + cell * S::TRANS + q * NB * D;
-#pragma unroll
-      for (int bb = 0; bb < NB; ++bb)
+      if constexpr (STD) {
+        // T[0][k] = ((0 + (-1)J0k) + (-1)J1k) + (-1)J2k  ==  (-J0k - J1k) - J2k  (up to the sign of 0)
+        // T[b][k] = ((0 + 0 J0k) + 1 J1k) + 0 J2k ...     ==  J[b-1][k]          (up to the sign of 0)
 #pragma unroll
         for (int k = 0; k < D; ++k) {
-          T acc = T(0);
+          T acc = -J[k];
 #pragma unroll
-          for (int j = 0; j < D; ++j) acc = add(acc, mul(Dq[bb * D + j], J[j * D + k]));
-          tr[bb][k] = acc;
-          trans_out[bb * D + k] = acc;
+          for (int j = 1; j < D; ++j) acc = add(acc, -J[j * D + k]);
+          tr[0][k] = acc;
         }
+#pragma unroll
+        for (int bb = 1; bb < NB; ++bb)
+#pragma unroll
+          for (int k = 0; k < D; ++k) tr[bb][k] = J[(bb - 1) * D + k];
+        if (q == 0) {
+#pragma unroll
+          for (int k = 0; k < D; ++k) s_tr[lc * S::TRS + k] = tr[0][k];
+        }
+      } else {
+        const T* Dq = tab.D + q * NB * D;
+#pragma unroll
+        for (int bb = 0; bb < NB; ++bb)
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            T acc = mul(Dq[bb * D], J[k]);
+#pragma unroll
+            for (int j = 1; j < D; ++j) acc = add(acc, mul(Dq[bb * D + j], J[j * D + k]));
+            tr[bb][k] = acc;
+            s_tr[lc * S::TRS + (q * NB + bb) * D + k] = acc;
+          }
+      }
 
       T g[NCOMP][D];
 #pragma unroll
       for (int c = 0; c < NCOMP; ++c)
 #pragma unroll
-        for (int k = 0; k < D; ++k) g[c][k] = T(0);
+        for (int k = 0; k < D; ++k) {
+          T acc = mul(cf[c], tr[0][k]);
 #pragma unroll
-      for (int bb = 0; bb < NB; ++bb)
-#pragma unroll
-        for (int c = 0; c < NCOMP; ++c)
-#pragma unroll
-          for (int k = 0; k < D; ++k) g[c][k] = add(g[c][k], mul(cf[bb * NCOMP + c], tr[bb][k]));
+          for (int bb = 1; bb < NB; ++bb) acc = add(acc, mul(cf[bb * NCOMP + c], tr[bb][k]));
+          g[c][k] = acc;
+        }
 
       T a0 = T(0);
       if constexpr (AUX == 1) {
         a0 = s_aux[cell];
       } else if constexpr (AUX == 2) {
+        T av[NB];
+        load_row<T, NB, VEC>(s_aux + cell * AUXW, av);
+        const T* Bq = tab.B + q * NB;
+        a0 = mul(av[0], Bq[0]);
 #pragma unroll
-        for (int bb = 0; bb < NB; ++bb) a0 = add(a0, mul(s_aux[cell * NB + bb], Bq[bb]));
+        for (int bb = 1; bb < NB; ++bb) a0 = add(a0, mul(av[bb], Bq[bb]));
       }
-      (void)Bq;
       (void)a0;
 
-      const T wq = a.tab.W[q];
-      T* f1_out = s_f1s + cell * S::F1S + q * NCOMP * D;
+      const T wq = tab.W[q];
+      T* f1_out = s_f1 + lc * S::F1S + q * NCOMP * D;
 #pragma unroll
       for (int c = 0; c < NCOMP; ++c)
 #pragma unroll
@@ -278,30 +249,163 @@ integrate_kernel(const __grid_constant__ IntegrateArgs<T> a) {
           f1_out[c * D + k] = mul(mul(fv, det), wq);
         }
     }
+  }
 
-    __syncthreads();  // ==== transpose threads ====
+  __syncwarp();  // ==== transpose threads (warp scope) ====
 
-    // ------------- basis phase: thread <-> element entry (cell, b, c) -------------
-    T* out = a.out + c0 * NBC;
-    for (int o = tid; o < ncell * NBC; o += nt) {
-      const int cell = o / NBC;
-      const T* tr = s_trans + cell * S::TRANS + my_b * D;
-      const T* f1 = s_f1s + cell * S::F1S + my_c * D;
-      T e = T(0);
+  // ------------- basis phase: lane <-> element entry (cell, b, c) -------------
+  T* o_base = out + (int64_t)c0 * NBC;
+  auto entry = [&](int o) {
+    const int lc = o / NBC;
+    const int r = o - lc * NBC;
+    const int b = r / NCOMP;
+    const int c = r - b * NCOMP;
+    // f1s rows of this entry's component: one vector load when N_comp == 1
+    T f1[NQ * D];
+    if constexpr (NCOMP == 1 && S::F1S == NQ * D) {
+      load_row<T, NQ * D>(s_f1 + lc * S::F1S, f1);
+    } else {
 #pragma unroll
       for (int q = 0; q < NQ; ++q)
 #pragma unroll
-        for (int k = 0; k < D; ++k) e = add(e, mul(tr[q * NB * D + k], f1[q * NCOMP * D + k]));
-      out[o] = e;
+        for (int k = 0; k < D; ++k) f1[q * D + k] = s_f1[lc * S::F1S + (q * NCOMP + c) * D + k];
     }
+    T e = T(0);  // the output chain starts at +0 exactly as the reference's
+    if constexpr (STD) {
+      const T* tp = b == 0 ? s_tr + lc * S::TRS : s_inv + (c0 + lc) * DD + (b - 1) * D;
+      T t[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) t[k] = tp[k];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+#pragma unroll
+        for (int k = 0; k < D; ++k) e = add(e, mul(t[k], f1[q * D + k]));
+    } else {
+      const T* tp = s_tr + lc * S::TRS + b * D;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+#pragma unroll
+        for (int k = 0; k < D; ++k) e = add(e, mul(tp[q * NB * D + k], f1[q * D + k]));
+    }
+    o_base[o] = e;
+  };
+  constexpr int FULL = S::CW * NBC;
+  if (nc == S::CW && FULL % 32 == 0) {
+#pragma unroll
+    for (int s = 0; s < FULL / 32; ++s) entry(s * 32 + lane);
+  } else {
+    for (int o = lane; o < nc * NBC; o += 32) entry(o);
+  }
+  __syncwarp();  // scratch is reused by the next slice
+}
 
-    __syncthreads();  // stage and scratch free again
-    if (tid == 0) issue(i + a.stages);
+template <typename T, int D, int NQ, int NCOMP, int FORM, int AUX, bool STD>
+__global__ void __launch_bounds__(MAX_CTA_THREADS, 1)
+integrate_kernel(const __grid_constant__ IntegrateArgs<T> a) {
+  constexpr int NB = D + 1, DD = D * D, NBC = NB * NCOMP;
+  using L = StageLayout<T, D, NCOMP, AUX>;
+  using S = Scratch<T, D, NQ, NCOMP, STD>;
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int nbc = a.n_bc;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int W = a.warps;
+  const int stage_bytes = L::stage_bytes(nbc);
+  unsigned char* scratch_base = smem + a.stages * stage_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(scratch_base + W * S::BYTES);
+  uint64_t* empty = full + a.stages;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], W);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // A batch may arrive by bulk copy when its four slices are 16-byte aligned
+  // and 16-byte sized (chunk starts are multiples of 16 cells, N_bc*s*k % 16
+  // is checked on the host; only a chunk's last, partial batch can fail).
+  auto bulk_ok = [&](int ncell) {
+    if (!a.bulk) return false;
+    if (ncell == nbc) return true;
+    return ((int64_t)ncell * sizeof(T) % 16 == 0) && ((int64_t)ncell * DD * sizeof(T) % 16 == 0) &&
+           ((int64_t)ncell * NBC * sizeof(T) % 16 == 0) && ((int64_t)ncell * L::AUXW * sizeof(T) % 16 == 0);
+  };
+
+  if (warp == W) {
+    // ============================ producer warp ============================
+    if (lane != 0) return;
+    const uint64_t policy = l2_evict_first_policy();
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t ci = blockIdx.x; ci < a.n_chunks; ci += gridDim.x) {
+      const int64_t lo = ci * a.chunk_cells;
+      const int64_t hi = lo + a.chunk_cells < a.n_cells ? lo + a.chunk_cells : a.n_cells;
+      for (int64_t c0 = lo; c0 < hi; c0 += nbc) {
+        const int ncell = hi - c0 < nbc ? (int)(hi - c0) : nbc;
+        if (!bulk_ok(ncell)) continue;  // consumers read this batch from global
+        mbar_wait(&empty[stage], phase ^ 1);
+        unsigned char* st = smem + stage * stage_bytes;
+        const uint32_t ib = ncell * DD * sizeof(T), db = ncell * sizeof(T), cb = ncell * NBC * sizeof(T),
+                       ab = ncell * L::AUXW * sizeof(T);
+        mbar_arrive_expect_tx(&full[stage], ib + db + cb + ab);
+        bulk_g2s(st, a.inv_j + c0 * DD, ib, &full[stage], policy);
+        bulk_g2s(st + L::inv_bytes(nbc), a.det_j + c0, db, &full[stage], policy);
+        bulk_g2s(st + L::inv_bytes(nbc) + L::det_bytes(nbc), a.coeffs + c0 * NBC, cb, &full[stage], policy);
+        if constexpr (AUX != 0)
+          bulk_g2s(st + L::inv_bytes(nbc) + L::det_bytes(nbc) + L::coef_bytes(nbc), a.aux + c0 * L::AUXW, ab,
+                   &full[stage], policy);
+        if (++stage == a.stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    return;
+  }
+
+  // ============================ consumer warps ============================
+  unsigned char* scratch = scratch_base + warp * S::BYTES;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int64_t ci = blockIdx.x; ci < a.n_chunks; ci += gridDim.x) {
+    const int64_t lo = ci * a.chunk_cells;
+    const int64_t hi = lo + a.chunk_cells < a.n_cells ? lo + a.chunk_cells : a.n_cells;
+    for (int64_t c0 = lo; c0 < hi; c0 += nbc) {
+      const int ncell = hi - c0 < nbc ? (int)(hi - c0) : nbc;
+      T* out = a.out + c0 * NBC;
+      if (bulk_ok(ncell)) {
+        mbar_wait(&full[stage], phase);
+        const unsigned char* st = smem + stage * stage_bytes;
+        const T* s_inv = reinterpret_cast<const T*>(st);
+        const T* s_det = reinterpret_cast<const T*>(st + L::inv_bytes(nbc));
+        const T* s_coef = reinterpret_cast<const T*>(st + L::inv_bytes(nbc) + L::det_bytes(nbc));
+        const T* s_aux =
+            reinterpret_cast<const T*>(st + L::inv_bytes(nbc) + L::det_bytes(nbc) + L::coef_bytes(nbc));
+        for (int c = warp * S::CW; c < ncell; c += W * S::CW)
+          warp_slice<T, D, NQ, NCOMP, FORM, AUX, STD, true>(a.tab, s_inv, s_det, s_coef, s_aux, scratch, c,
+                                                           ncell, out, lane);
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == a.stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      } else {
+        // unaligned caller buffers or an odd-sized last batch: read straight from global memory
+        const T* g_aux = AUX != 0 ? a.aux + c0 * L::AUXW : nullptr;
+        for (int c = warp * S::CW; c < ncell; c += W * S::CW)
+          warp_slice<T, D, NQ, NCOMP, FORM, AUX, STD, false>(a.tab, a.inv_j + c0 * DD, a.det_j + c0,
+                                                            a.coeffs + c0 * NBC, g_aux, scratch, c, ncell, out,
+                                                            lane);
+      }
+    }
   }
 }
 
 // ---------------------------------------------------------------------------
-// Host side: launch geometry, dispatch, C ABI.
+// Host side: launch geometry, dispatch.
 // ---------------------------------------------------------------------------
 
 struct Config {
@@ -309,8 +413,8 @@ struct Config {
 };
 
 struct Geometry {
-  int n_bl, n_cb, n_bc, n_t, threads, stages, smem, grid;
-  int64_t n_batches, n_chunks;
+  int n_bl, n_cb, n_bc, n_t, threads, warps, stages, smem, grid;
+  int64_t n_chunks, chunk_cells;
 };
 
 static int env_int(const char* name, int dflt) {
@@ -335,53 +439,66 @@ int validate(const Config& c) {
                   (c.form == 1 && (c.aux == 1 || c.aux == 2) && c.n_comp == 1) ||
                   (c.form == 2 && c.aux == 0 && c.n_comp == c.dim);
   if (!ok) {
-    set_error("cuda lane does not cover form_code=%d aux_mode=%d n_comp=%d dim=%d", c.form,
-              c.aux, c.n_comp, c.dim);
+    set_error("cuda lane does not cover form_code=%d aux_mode=%d n_comp=%d dim=%d", c.form, c.aux, c.n_comp,
+              c.dim);
     return TXB_E_UNSUPPORTED;
   }
   return TXB_OK;
 }
 
-// Tuned defaults (B200): N_bc*N_comp = N_t near 256-384 threads.
+static int gcd(int a, int b) { return b ? gcd(b, a % b) : a; }
+
+// Default N_bl: batch near TXB_TARGET_CELLS (256) cells, N_bc a multiple of
+// the warp slice CW = 32/N_q so no warp slice is partial.
 static void default_decomposition(const Config& c, int& n_bl, int& n_cb) {
-  const int nb = c.dim + 1;
+  const int nbs = (c.dim + 1) * c.n_q;
   if (n_bl <= 0) {
-    const int target = env_int("TXB_TARGET_THREADS", 256);
-    n_bl = std::max(1, target / (nb * c.n_q * c.n_comp));
-    // keep N_bc a multiple of 4 cells so every batch slice is 16-byte sized
-    while ((n_bl * nb * c.n_q) % 4 != 0) ++n_bl;
+    const int cw = 32 / c.n_q;
+    const int step = cw / gcd(cw, nbs);  // n_bl multiple of step -> N_bc multiple of cw
+    const int target = env_int("TXB_TARGET_CELLS", 256);
+    int best = step, best_err = 1 << 30;
+    for (int m = 1; m * step * nbs <= 1024; ++m) {
+      const int err = std::abs(m * step * nbs - target);
+      if (err < best_err) {
+        best_err = err;
+        best = m * step;
+      }
+    }
+    n_bl = best;
   }
-  if (n_cb <= 0) n_cb = env_int("TXB_DEFAULT_NCB", 1);
+  if (n_cb <= 0) n_cb = env_int("TXB_DEFAULT_NCB", 0);  // 0: balanced contiguous chunks
 }
 
-template <typename T, int D, int NQ, int NCOMP, int FORM, int AUX>
+template <typename T, int D, int NQ, int NCOMP, int FORM, int AUX, bool STD>
 struct Kernel {
   using L = StageLayout<T, D, NCOMP, AUX>;
-  static void* fn() { return (void*)integrate_kernel<T, D, NQ, NCOMP, FORM, AUX>; }
+  static void* fn() { return (void*)integrate_kernel<T, D, NQ, NCOMP, FORM, AUX, STD>; }
   static int stage_bytes(int n_bc) { return L::stage_bytes(n_bc); }
-  static int scratch(int n_bc) { return scratch_bytes<T, D, NQ, NCOMP>(n_bc); }
+  static int scratch(int) { return Scratch<T, D, NQ, NCOMP, STD>::BYTES; }
+  static constexpr int CW = 32 / NQ;
 };
 
 struct KernelInfo {
   void* fn;
   int (*stage_bytes)(int);
-  int (*scratch)(int);
+  int (*scratch)(int);  // per consumer warp
+  int cw;
 };
 
-template <typename T, int D, int NQ>
+template <typename T, int D, int NQ, bool STD>
 static bool pick_form(const Config& c, KernelInfo& k) {
   if (c.form == 0) {
-    using K = Kernel<T, D, NQ, 1, 0, 0>;
-    k = {K::fn(), K::stage_bytes, K::scratch};
+    using K = Kernel<T, D, NQ, 1, 0, 0, STD>;
+    k = {K::fn(), K::stage_bytes, K::scratch, K::CW};
   } else if (c.form == 1 && c.aux == 1) {
-    using K = Kernel<T, D, NQ, 1, 1, 1>;
-    k = {K::fn(), K::stage_bytes, K::scratch};
+    using K = Kernel<T, D, NQ, 1, 1, 1, STD>;
+    k = {K::fn(), K::stage_bytes, K::scratch, K::CW};
   } else if (c.form == 1 && c.aux == 2) {
-    using K = Kernel<T, D, NQ, 1, 1, 2>;
-    k = {K::fn(), K::stage_bytes, K::scratch};
+    using K = Kernel<T, D, NQ, 1, 1, 2, STD>;
+    k = {K::fn(), K::stage_bytes, K::scratch, K::CW};
   } else if (c.form == 2) {
-    using K = Kernel<T, D, NQ, D, 2, 0>;
-    k = {K::fn(), K::stage_bytes, K::scratch};
+    using K = Kernel<T, D, NQ, D, 2, 0, STD>;
+    k = {K::fn(), K::stage_bytes, K::scratch, K::CW};
   } else {
     return false;
   }
@@ -389,23 +506,50 @@ static bool pick_form(const Config& c, KernelInfo& k) {
 }
 
 template <typename T, int D>
-static bool pick_nq(const Config& c, KernelInfo& k) {
+static bool pick_nq(const Config& c, bool std_tab, KernelInfo& k) {
+  if (std_tab) {  // standard P1 tables: midpoint and two-point rules
+    if (c.n_q == 1) return pick_form<T, D, 1, true>(c, k);
+    if (c.n_q == 2) return pick_form<T, D, 2, true>(c, k);
+  }
   switch (c.n_q) {
-    case 1: return pick_form<T, D, 1>(c, k);
-    case 2: return pick_form<T, D, 2>(c, k);
-    case 3: return pick_form<T, D, 3>(c, k);
-    case 4: return pick_form<T, D, 4>(c, k);
-    case 5: return pick_form<T, D, 5>(c, k);
-    case 6: return pick_form<T, D, 6>(c, k);
-    case 7: return pick_form<T, D, 7>(c, k);
-    case 8: return pick_form<T, D, 8>(c, k);
+    case 1: return pick_form<T, D, 1, false>(c, k);
+    case 2: return pick_form<T, D, 2, false>(c, k);
+    case 3: return pick_form<T, D, 3, false>(c, k);
+    case 4: return pick_form<T, D, 4, false>(c, k);
+    case 5: return pick_form<T, D, 5, false>(c, k);
+    case 6: return pick_form<T, D, 6, false>(c, k);
+    case 7: return pick_form<T, D, 7, false>(c, k);
+    case 8: return pick_form<T, D, 8, false>(c, k);
   }
   return false;
 }
 
-static bool pick_kernel(const Config& c, KernelInfo& k) {
-  if (c.dtype == 4) return c.dim == 2 ? pick_nq<float, 2>(c, k) : pick_nq<float, 3>(c, k);
-  return c.dim == 2 ? pick_nq<double, 2>(c, k) : pick_nq<double, 3>(c, k);
+static bool pick_kernel(const Config& c, bool std_tab, KernelInfo& k) {
+  if (env_int("TXB_DISABLE_STD", 0)) std_tab = false;
+  if (c.dtype == 4) return c.dim == 2 ? pick_nq<float, 2>(c, std_tab, k) : pick_nq<float, 3>(c, std_tab, k);
+  return c.dim == 2 ? pick_nq<double, 2>(c, std_tab, k) : pick_nq<double, 3>(c, std_tab, k);
+}
+
+// True when every tabulated reference gradient is exactly the P1 one:
+// D[q][0][j] = -1, D[q][b][j] = (b-1 == j) for b >= 1 (element.py:55-77).
+template <typename T>
+static bool is_standard_p1(const void* basis_der, int n_q, int d) {
+  const T* D = (const T*)basis_der;
+  const int nb = d + 1;
+  for (int q = 0; q < n_q; ++q)
+    for (int b = 0; b < nb; ++b)
+      for (int j = 0; j < d; ++j) {
+        const T want = b == 0 ? T(-1) : (b - 1 == j ? T(1) : T(0));
+        const T got = D[(q * nb + b) * d + j];
+        if (memcmp(&got, &want, sizeof(T)) != 0) return false;  // bitwise (no -0)
+      }
+  return true;
+}
+
+static bool standard_tables(const Config& c, const void* basis_der) {
+  if (!basis_der) return false;
+  return c.dtype == 4 ? is_standard_p1<float>(basis_der, c.n_q, c.dim)
+                      : is_standard_p1<double>(basis_der, c.n_q, c.dim);
 }
 
 struct DeviceProps {
@@ -424,18 +568,18 @@ static DeviceProps device_props(int dev) {
   return cache[dev];
 }
 
-static int compute_geometry(const Config& c, const KernelInfo& k, int64_t n_cells, int n_bl,
-                            int n_cb, bool query_device, Geometry& g) {
+static int compute_geometry(const Config& c, const KernelInfo& k, int64_t n_cells, int n_bl, int n_cb,
+                            bool query_device, Geometry& g) {
   default_decomposition(c, n_bl, n_cb);
   const int nb = c.dim + 1;
   const int64_t n_bc64 = (int64_t)n_bl * nb * c.n_q;
   const int64_t n_t64 = n_bc64 * c.n_comp;
-  if (n_bl < 1 || n_cb < 1) {
-    set_error("n_bl and n_cb must be >= 1 (got %d, %d)", n_bl, n_cb);
+  if (n_bl < 1 || n_cb < 0) {
+    set_error("n_bl must be >= 1 and n_cb >= 1 (got %d, %d)", n_bl, n_cb);
     return TXB_E_CONFIG;
   }
   if (n_t64 > TXB_THREAD_LIMIT) {
-    // txfem/schedule.py:86-90: the thread block may not exceed the device limit.
+    // txfem/schedule.py:86-90: the paper's thread block may not exceed the device limit.
     set_error("thread block needs %lld threads, device limit is %d (n_bs=%d * n_comp=%d * n_bl=%d)",
               (long long)n_t64, TXB_THREAD_LIMIT, nb * c.n_q, c.n_comp, n_bl);
     return TXB_E_CONFIG;
@@ -444,22 +588,13 @@ static int compute_geometry(const Config& c, const KernelInfo& k, int64_t n_cell
   g.n_cb = n_cb;
   g.n_bc = (int)n_bc64;
   g.n_t = (int)n_t64;
-  // Physical CTA size: N_t, or the largest multiple of N_b*N_comp dividing it
-  // that fits MAX_CTA_THREADS (same work items, walked in more steps).
-  const int unit = nb * c.n_comp;
-  int threads = g.n_t;
-  if (threads > MAX_CTA_THREADS) {
-    int best = unit;
-    for (int m = unit; m <= MAX_CTA_THREADS; m += unit)
-      if (g.n_t % m == 0) best = m;
-    threads = best;
-  }
-  g.threads = threads;
-  g.n_batches = (n_cells + g.n_bc - 1) / g.n_bc;
-  g.n_chunks = (g.n_batches + n_cb - 1) / n_cb;
+  const int slices = (g.n_bc + k.cw - 1) / k.cw;
+  const int wcap = std::max(1, std::min(MAX_CONSUMER_WARPS, env_int("TXB_MAX_WARPS", MAX_CONSUMER_WARPS)));
+  g.warps = std::min(wcap, slices);
+  g.threads = 32 * (g.warps + 1);
 
   const int stage = k.stage_bytes(g.n_bc);
-  const int fixed = k.scratch(g.n_bc) + 8 * 8;  // scratch + up to 8 mbarriers
+  const int fixed = g.warps * k.scratch(g.n_bc) + 16 * 8;  // scratch + 2*8 mbarriers
   int smem_cap = 227 * 1024;
   int dev = 0, sms = 148;
   if (query_device && cudaGetDevice(&dev) == cudaSuccess) {
@@ -467,14 +602,14 @@ static int compute_geometry(const Config& c, const KernelInfo& k, int64_t n_cell
     if (p.smem_optin > 0) smem_cap = p.smem_optin;
     if (p.sms > 0) sms = p.sms;
   }
-  const int target = env_int("TXB_SMEM_TARGET", 100 * 1024);
+  const int target = env_int("TXB_SMEM_TARGET", 110 * 1024);
   int stages = env_int("TXB_STAGES", 0);
   if (stages <= 0) stages = std::min(8, std::max(2, (target - fixed) / std::max(stage, 1)));
   stages = std::min(stages, 8);
   while (stages > 2 && fixed + stages * stage > smem_cap) --stages;
   if (fixed + stages * stage > smem_cap) {
-    set_error("shared-memory image needs %d bytes, budget is %d (n_bl=%d, scalar width %d)",
-              fixed + 2 * stage, smem_cap, n_bl, c.dtype);
+    set_error("shared-memory image needs %d bytes, budget is %d (n_bl=%d, scalar width %d)", fixed + 2 * stage,
+              smem_cap, n_bl, c.dtype);
     return TXB_E_CAPACITY;
   }
   g.stages = stages;
@@ -485,20 +620,30 @@ static int compute_geometry(const Config& c, const KernelInfo& k, int64_t n_cell
     static std::mutex mu;
     std::lock_guard<std::mutex> lk(mu);
     cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.fn, g.threads, g.smem) != cudaSuccess ||
-        occ < 1)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.fn, g.threads, g.smem) != cudaSuccess || occ < 1)
       occ = 1;
   } else {
     occ = std::max(1, std::min(2048 / g.threads, smem_cap / std::max(g.smem, 1)));
   }
   const int64_t resident = (int64_t)occ * sms;
+  if (n_cb > 0) {
+    // paper mode: chunks of N_cb batches, round-robin over the CTAs
+    g.chunk_cells = (int64_t)n_cb * g.n_bc;
+  } else {
+    // balanced mode: one contiguous chunk per resident CTA, 16-cell granular
+    // (keeps every bulk-copy slice 16-byte aligned), so all CTAs finish together
+    const int64_t per = (n_cells + resident - 1) / std::max<int64_t>(resident, 1);
+    g.chunk_cells = std::max<int64_t>(16, (per + 15) / 16 * 16);
+    g.n_cb = (int)((g.chunk_cells + g.n_bc - 1) / g.n_bc);
+  }
+  g.n_chunks = (n_cells + g.chunk_cells - 1) / g.chunk_cells;
   g.grid = (int)std::max<int64_t>(1, std::min<int64_t>(g.n_chunks, resident));
   return TXB_OK;
 }
 
 template <typename T>
-static void fill_tab(Tabulation<T>& t, int n_q, int n_b, int d, const void* basis,
-                     const void* basis_der, const void* weights) {
+static void fill_tab(Tabulation<T>& t, int n_q, int n_b, int d, const void* basis, const void* basis_der,
+                     const void* weights) {
   memset(&t, 0, sizeof(t));
   memcpy(t.B, basis, sizeof(T) * n_q * n_b);
   memcpy(t.D, basis_der, sizeof(T) * n_q * n_b * d);
@@ -506,10 +651,9 @@ static void fill_tab(Tabulation<T>& t, int n_q, int n_b, int d, const void* basi
 }
 
 template <typename T>
-static int launch_t(const Config& c, const KernelInfo& k, const Geometry& g, int64_t n_cells,
-                    const void* basis, const void* basis_der, const void* weights,
-                    const void* inv_j, const void* det_j, const void* coeffs, const void* aux,
-                    void* out, cudaStream_t stream) {
+static int launch_t(const Config& c, const KernelInfo& k, const Geometry& g, int64_t n_cells, const void* basis,
+                    const void* basis_der, const void* weights, const void* inv_j, const void* det_j,
+                    const void* coeffs, const void* aux, void* out, cudaStream_t stream) {
   IntegrateArgs<T> a;
   a.inv_j = (const T*)inv_j;
   a.det_j = (const T*)det_j;
@@ -517,13 +661,19 @@ static int launch_t(const Config& c, const KernelInfo& k, const Geometry& g, int
   a.aux = (const T*)aux;
   a.out = (T*)out;
   a.n_cells = n_cells;
-  a.n_batches = g.n_batches;
   a.n_chunks = g.n_chunks;
+  a.chunk_cells = g.chunk_cells;
   a.n_bc = g.n_bc;
-  a.n_cb = g.n_cb;
   a.stages = g.stages;
+  a.warps = g.warps;
+  // Bulk copies need 16-byte aligned, 16-byte sized slices for EVERY batch:
+  // aligned base pointers and N_bc * (per-cell scalars) * sizeof(T) % 16 == 0
+  // for each of the four arrays.  Otherwise every batch is read from global.
   auto al16 = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
-  a.bulk = al16(inv_j) && al16(det_j) && al16(coeffs) && (c.aux == 0 || al16(aux)) &&
+  const int nb = c.dim + 1, auxw = c.aux == 1 ? 1 : (c.aux == 2 ? nb : 0);
+  auto sized16 = [&](int per_cell) { return ((int64_t)g.n_bc * per_cell * (int64_t)sizeof(T)) % 16 == 0; };
+  a.bulk = al16(inv_j) && al16(det_j) && al16(coeffs) && (c.aux == 0 || al16(aux)) && sized16(c.dim * c.dim) &&
+           sized16(1) && sized16(nb * c.n_comp) && (c.aux == 0 || sized16(auxw)) &&
            env_int("TXB_DISABLE_BULK", 0) == 0;
   fill_tab(a.tab, c.n_q, c.dim + 1, c.dim, basis, basis_der, weights);
   void* params[] = {&a};
@@ -531,10 +681,9 @@ static int launch_t(const Config& c, const KernelInfo& k, const Geometry& g, int
   return TXB_OK;
 }
 
-int integrate_device(const Config& c, int n_b, int64_t n_cells, const void* basis,
-                     const void* basis_der, const void* weights, const void* inv_j,
-                     const void* det_j, const void* coeffs, const void* aux, void* out, int n_bl,
-                     int n_cb, cudaStream_t stream) {
+int integrate_device(const Config& c, int n_b, int64_t n_cells, const void* basis, const void* basis_der,
+                     const void* weights, const void* inv_j, const void* det_j, const void* coeffs,
+                     const void* aux, void* out, int n_bl, int n_cb, cudaStream_t stream) {
   int rc = validate(c);
   if (rc) return rc;
   if (n_b != c.dim + 1) {
@@ -550,7 +699,7 @@ int integrate_device(const Config& c, int n_b, int64_t n_cells, const void* basi
     return TXB_E_ARG;
   }
   KernelInfo k;
-  if (!pick_kernel(c, k)) {
+  if (!pick_kernel(c, standard_tables(c, basis_der), k)) {
     set_error("no kernel instantiation for this configuration");
     return TXB_E_UNSUPPORTED;
   }
@@ -563,10 +712,8 @@ int integrate_device(const Config& c, int n_b, int64_t n_cells, const void* basi
     return TXB_E_ARG;
   }
   if (c.dtype == 4)
-    return launch_t<float>(c, k, g, n_cells, basis, basis_der, weights, inv_j, det_j, coeffs, aux,
-                           out, stream);
-  return launch_t<double>(c, k, g, n_cells, basis, basis_der, weights, inv_j, det_j, coeffs, aux,
-                          out, stream);
+    return launch_t<float>(c, k, g, n_cells, basis, basis_der, weights, inv_j, det_j, coeffs, aux, out, stream);
+  return launch_t<double>(c, k, g, n_cells, basis, basis_der, weights, inv_j, det_j, coeffs, aux, out, stream);
 }
 
 // ---------------------------------------------------------------------------
@@ -671,15 +818,22 @@ int integrate_host(const Config& c, int n_b, int64_t n_cells, const void* basis,
 // grid-stride; the write value depends on the reads so nothing is elided.
 __global__ void stream_probe_kernel(const uint4* __restrict__ src, int64_t n_read,
                                     uint4* __restrict__ dst, int64_t n_write) {
+  constexpr int U = 8;  // independent 16-byte loads in flight per thread
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = n_read > n_write ? n_read : n_write;
-  uint32_t acc = 0;
-  for (int64_t i = t0; i < n; i += stride) {
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (i < n_read) v = __ldcs(src + i);
-    acc ^= v.x ^ v.y ^ v.z ^ v.w;
-    if (i < n_write) __stcs(dst + i, make_uint4(v.x, v.y, v.z, acc));
+  for (int64_t base = t0; base < n; base += stride * U) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + u * stride;
+      v[u] = i < n_read ? __ldcs(src + i) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + u * stride;
+      if (i < n_write) __stcs(dst + i, v[u]);
+    }
   }
 }
 
@@ -705,8 +859,8 @@ extern "C" int txb_launch_config(int form_code, int aux_mode, int dtype_bytes, i
   Config c{form_code, aux_mode, dtype_bytes, dim, n_q, n_comp};
   int rc = validate(c);
   if (rc) return rc;
-  KernelInfo k;
-  if (!pick_kernel(c, k)) return TXB_E_UNSUPPORTED;
+  KernelInfo k;  // reports the standard-P1-table kernel's geometry
+  if (!pick_kernel(c, true, k)) return TXB_E_UNSUPPORTED;
   int ndev = 0;
   const bool have_dev = cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0;
   if (!have_dev) cudaGetLastError();
@@ -753,8 +907,10 @@ extern "C" int txb_stream_probe(const void* src, int64_t read_bytes, void* dst,
   int dev = 0;
   TXB_CUDA_TRY(cudaGetDevice(&dev));
   const DeviceProps p = device_props(dev);
-  const int grid = std::max(1, p.sms) * 8;
-  stream_probe_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+  const int grid = std::max(1, p.sms) * 4;
+  // 4 x 512-thread CTAs per SM, 8 loads each in flight
+
+  stream_probe_kernel<<<grid, 512, 0, (cudaStream_t)stream>>>(
       (const uint4*)src, read_bytes / 16, (uint4*)dst, write_bytes / 16);
   TXB_CUDA_TRY(cudaGetLastError());
   return TXB_OK;

@@ -158,9 +158,9 @@ def test_host_path_matches_device_path():
 def test_output_fully_overwritten_and_inputs_untouched():
     B, D, W = oracle.p1_tables(2)
     full, inv, det, coeffs, aux = oracle.workload(2, "elasticity", 10_000, seed=4)
-    ti = torch.from_numpy(inv).cuda()
-    td = torch.from_numpy(det).cuda()
-    tc = torch.from_numpy(coeffs).cuda()
+    ti = torch.from_numpy(np.ascontiguousarray(inv)).cuda()
+    td = torch.from_numpy(np.ascontiguousarray(det)).cuda()
+    tc = torch.from_numpy(np.ascontiguousarray(coeffs)).cuda()
     snap = [t.clone() for t in (ti, td, tc)]
     out = torch.full(tuple(coeffs.shape), float("nan"), dtype=torch.float64, device="cuda")
     backend.run_cuda((2, 0), B, D, W, ti, td, tc, None, out)

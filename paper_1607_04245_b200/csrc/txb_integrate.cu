@@ -40,7 +40,9 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <vector>
 
 namespace txb {
@@ -323,6 +325,12 @@ integrate_kernel(const __grid_constant__ IntegrateArgs<T> a) {
     fence_mbar_init();
   }
   __syncthreads();
+  // Programmatic dependent launch: everything above overlapped the previous
+  // grid in the stream; from here on we touch global memory, so wait for it
+  // (no-op when launched without the PDL attribute), then let the next grid
+  // start its own prologue as our CTAs retire.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // A batch may arrive by bulk copy when its four slices are 16-byte aligned
   // and 16-byte sized (chunk starts are multiples of 16 cells, N_bc*s*k % 16
@@ -455,7 +463,7 @@ static void default_decomposition(const Config& c, int& n_bl, int& n_cb) {
   if (n_bl <= 0) {
     const int cw = 32 / c.n_q;
     const int step = cw / gcd(cw, nbs);  // n_bl multiple of step -> N_bc multiple of cw
-    const int target = env_int("TXB_TARGET_CELLS", 256);
+    const int target = env_int("TXB_TARGET_CELLS", c.dtype == 8 ? 128 : 256);
     int best = step, best_err = 1 << 30;
     for (int m = 1; m * step * nbs <= 1024; ++m) {
       const int err = std::abs(m * step * nbs - target);
@@ -602,28 +610,77 @@ static int compute_geometry(const Config& c, const KernelInfo& k, int64_t n_cell
     if (p.smem_optin > 0) smem_cap = p.smem_optin;
     if (p.sms > 0) sms = p.sms;
   }
-  const int target = env_int("TXB_SMEM_TARGET", 110 * 1024);
-  int stages = env_int("TXB_STAGES", 0);
-  if (stages <= 0) stages = std::min(8, std::max(2, (target - fixed) / std::max(stage, 1)));
-  stages = std::min(stages, 8);
-  while (stages > 2 && fixed + stages * stage > smem_cap) --stages;
-  if (fixed + stages * stage > smem_cap) {
+  // Ring depth: keep about TXB_INFLIGHT_KB (72 KB) of batch loads in flight
+  // per SM -- (CTAs/SM) x (stages-1) x stage bytes ~ HBM bandwidth x latency
+  // per SM.  Deeper rings only queue more requests and lengthen the launch
+  // ramp (measured, profiles/r1_sweep.md).  TXB_STAGES forces a depth.
+  const int forced = env_int("TXB_STAGES", 0);
+  const int64_t inflight_target = (int64_t)env_int("TXB_INFLIGHT_KB", 72) * 1024;
+  auto occupancy = [&](int smem) {
+    int occ = 1;
+    if (query_device) {
+      static std::mutex mu;
+      std::lock_guard<std::mutex> lk(mu);
+      cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.fn, g.threads, smem) != cudaSuccess || occ < 1)
+        occ = 1;
+    } else {
+      occ = std::max(1, std::min(2048 / g.threads, smem_cap / std::max(smem, 1)));
+    }
+    return occ;
+  };
+  int best_s = -1, occ = 1;
+  int64_t best_err = -1;
+  // the choice depends only on the kernel shape: memoise it (the occupancy
+  // queries cost microseconds of host time per launch otherwise)
+  struct Key {
+    void* fn;
+    int threads, stage, fixed, forced, dev;
+    int64_t target;
+    bool operator<(const Key& o) const {
+      return std::tie(fn, threads, stage, fixed, forced, dev, target) <
+             std::tie(o.fn, o.threads, o.stage, o.fixed, o.forced, o.dev, o.target);
+    }
+  };
+  static std::mutex memo_mu;
+  static std::map<Key, std::pair<int, int>> memo;
+  const Key key{k.fn, g.threads, stage, fixed, forced, query_device ? dev : -1, inflight_target};
+  {
+    std::lock_guard<std::mutex> lk(memo_mu);
+    auto it = memo.find(key);
+    if (it != memo.end()) {
+      best_s = it->second.first;
+      occ = it->second.second;
+    }
+  }
+  const bool memoised = best_s >= 0;
+  for (int st = 2; !memoised && st <= 8; ++st) {
+    if (forced > 0 && st != std::min(std::max(forced, 2), 8)) continue;
+    const int smem = fixed + st * stage;
+    if (smem > smem_cap) break;
+    const int o = occupancy(smem);
+    const int64_t err = std::llabs((int64_t)o * (st - 1) * stage - inflight_target);
+    if (best_s < 0 || err < best_err) {
+      best_s = st;
+      best_err = err;
+      occ = o;
+    }
+  }
+  if (best_s < 0) {
     set_error("shared-memory image needs %d bytes, budget is %d (n_bl=%d, scalar width %d)", fixed + 2 * stage,
               smem_cap, n_bl, c.dtype);
     return TXB_E_CAPACITY;
   }
-  g.stages = stages;
-  g.smem = fixed + stages * stage;
-
-  int occ = 1;
+  if (!memoised) {
+    std::lock_guard<std::mutex> lk(memo_mu);
+    memo[key] = {best_s, occ};
+  }
+  g.stages = best_s;
+  g.smem = fixed + best_s * stage;
   if (query_device) {
-    static std::mutex mu;
-    std::lock_guard<std::mutex> lk(mu);
+    static std::mutex mu2;
+    std::lock_guard<std::mutex> lk(mu2);
     cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.fn, g.threads, g.smem) != cudaSuccess || occ < 1)
-      occ = 1;
-  } else {
-    occ = std::max(1, std::min(2048 / g.threads, smem_cap / std::max(g.smem, 1)));
   }
   const int64_t resident = (int64_t)occ * sms;
   if (n_cb > 0) {
@@ -677,7 +734,17 @@ static int launch_t(const Config& c, const KernelInfo& k, const Geometry& g, int
            env_int("TXB_DISABLE_BULK", 0) == 0;
   fill_tab(a.tab, c.n_q, c.dim + 1, c.dim, basis, basis_der, weights);
   void* params[] = {&a};
-  TXB_CUDA_TRY(cudaLaunchKernel(k.fn, dim3(g.grid), dim3(g.threads), params, (size_t)g.smem, stream));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g.grid);
+  cfg.blockDim = dim3(g.threads);
+  cfg.dynamicSmemBytes = (size_t)g.smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = env_int("TXB_PDL", 1) ? 1 : 0;
+  TXB_CUDA_TRY(cudaLaunchKernelExC(&cfg, k.fn, params));
   return TXB_OK;
 }
 

@@ -17,17 +17,21 @@ import bench  # noqa: E402
 def main():
     import torch
 
-    configs = sys.argv[1:] or ["3d_varcoef_f64", "3d_varcoef_f32", "3d_elasticity_f64", "2d_varcoef_f32"]
+    configs = sys.argv[1:] or ["3d_varcoef_f64", "3d_varcoef_f32", "3d_elasticity_f64", "3d_elasticity_f32", "2d_varcoef_f32",
+                               "2d_varcoef_f64", "2d_elasticity_f32"]
     peak, _ = bench.peaks()
     for name in configs:
         flops, bpc = bench.config_model(name)
         wl = bench.rank_workload(name, 0, 1)
         n_sets = max(4, -(-3 * bench.L2_BYTES // (bpc * wl["n"])) + 1)
         best = None
-        for threads, smem, stages in itertools.product([128, 256, 512], [48, 80, 110, 160, 220], [0]):
+        grid = [(c, sm, st, pdl) for c in (64, 128, 256) for sm in (40, 56, 80, 110) for st in (0,)
+                for pdl in (0, 1)]
+        for threads, smem, stages, pdl in grid:
             os.environ["TXB_TARGET_CELLS"] = str(threads)
             os.environ["TXB_SMEM_TARGET"] = str(smem * 1024)
             os.environ["TXB_STAGES"] = str(stages)
+            os.environ["TXB_PDL"] = str(pdl)
             try:
                 tot, _ = bench.time_device(wl, 200, 5, n_sets)
             except Exception as exc:  # capacity etc.
@@ -41,13 +45,13 @@ def main():
             w = 4 if wl["dtype"] == "f32" else 8
             cfg = backend.launch_config(*backend.cuda_kernel(form, 1, wl["aux"], w), w, wl["dim"], 1,
                                         form.n_comp, wl["n"])
-            rec = {"config": name, "cells": threads, "smem_kb": smem, "gbs": round(gbs, 1),
+            rec = {"config": name, "cells": threads, "smem_kb": smem, "pdl": pdl, "gbs": round(gbs, 1),
                    "frac": round(gbs / peak, 3), "us": round(ms * 1e3, 2), **cfg}
             print(json.dumps(rec), flush=True)
             if best is None or gbs > best["gbs"]:
                 best = rec
         print("BEST", json.dumps(best), flush=True)
-        for k in ("TXB_TARGET_CELLS", "TXB_SMEM_TARGET", "TXB_STAGES"):
+        for k in ("TXB_TARGET_CELLS", "TXB_SMEM_TARGET", "TXB_STAGES", "TXB_PDL"):
             os.environ.pop(k, None)
         del wl
         torch.cuda.empty_cache()

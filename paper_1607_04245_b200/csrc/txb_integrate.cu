@@ -38,6 +38,7 @@
 #include "txb_common.cuh"
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -49,6 +50,9 @@ namespace txb {
 
 constexpr int MAX_D = TXB_MAX_DIM, MAX_B = TXB_MAX_BASIS, MAX_Q = TXB_MAX_QUAD;
 constexpr int MAX_CONSUMER_WARPS = 16;
+constexpr int MAX_STAGES = 8;
+constexpr int WORK_POOL = 4096;  // per-launch dynamic-scheduling counters (device globals, zero at load)
+__device__ unsigned long long g_work_pool[WORK_POOL][2];
 constexpr int MAX_CTA_THREADS = 32 * (MAX_CONSUMER_WARPS + 1);
 
 template <typename T>
@@ -72,6 +76,8 @@ struct IntegrateArgs {
   int stages;  // ring depth
   int warps;   // consumer warps
   int bulk;    // 1: full batches arrive by bulk copy; 0: every batch read from global
+  unsigned long long* work;  // dynamic mode: {next batch, CTAs done}, self-resetting; NULL = static chunks
+  int64_t static_batches;    // dynamic mode: batches dealt round-robin before the counter takes over
   Tabulation<T> tab;
 };
 
@@ -315,9 +321,15 @@ integrate_kernel(const __grid_constant__ IntegrateArgs<T> a) {
   const int stage_bytes = L::stage_bytes(nbc);
   unsigned char* scratch_base = smem + a.stages * stage_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(scratch_base + W * S::BYTES);
-  uint64_t* empty = full + a.stages;
+  uint64_t* empty = full + MAX_STAGES;
+  // what the producer put in each stage: first cell and cell count (0 = stop),
+  // negative count = read this batch from global memory
+  int64_t* info_c0 = reinterpret_cast<int64_t*>(empty + MAX_STAGES);
+  int* info_n = reinterpret_cast<int*>(info_c0 + MAX_STAGES);
+  __shared__ int warps_done;
 
   if (threadIdx.x == 0) {
+    warps_done = 0;
     for (int s = 0; s < a.stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], W);
@@ -333,8 +345,8 @@ integrate_kernel(const __grid_constant__ IntegrateArgs<T> a) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // A batch may arrive by bulk copy when its four slices are 16-byte aligned
-  // and 16-byte sized (chunk starts are multiples of 16 cells, N_bc*s*k % 16
-  // is checked on the host; only a chunk's last, partial batch can fail).
+  // and 16-byte sized (N_bc*s*k % 16 and the base pointers are checked on the
+  // host; only a partial batch can fail the size test).
   auto bulk_ok = [&](int ncell) {
     if (!a.bulk) return false;
     if (ncell == nbc) return true;
@@ -348,13 +360,11 @@ integrate_kernel(const __grid_constant__ IntegrateArgs<T> a) {
     const uint64_t policy = l2_evict_first_policy();
     int stage = 0;
     uint32_t phase = 0;
-    for (int64_t ci = blockIdx.x; ci < a.n_chunks; ci += gridDim.x) {
-      const int64_t lo = ci * a.chunk_cells;
-      const int64_t hi = lo + a.chunk_cells < a.n_cells ? lo + a.chunk_cells : a.n_cells;
-      for (int64_t c0 = lo; c0 < hi; c0 += nbc) {
-        const int ncell = hi - c0 < nbc ? (int)(hi - c0) : nbc;
-        if (!bulk_ok(ncell)) continue;  // consumers read this batch from global
-        mbar_wait(&empty[stage], phase ^ 1);
+    auto publish = [&](int64_t c0, int ncell) {
+      mbar_wait(&empty[stage], phase ^ 1);
+      if (ncell > 0 && bulk_ok(ncell)) {
+        info_c0[stage] = c0;
+        info_n[stage] = ncell;
         unsigned char* st = smem + stage * stage_bytes;
         const uint32_t ib = ncell * DD * sizeof(T), db = ncell * sizeof(T), cb = ncell * NBC * sizeof(T),
                        ab = ncell * L::AUXW * sizeof(T);
@@ -365,12 +375,42 @@ integrate_kernel(const __grid_constant__ IntegrateArgs<T> a) {
         if constexpr (AUX != 0)
           bulk_g2s(st + L::inv_bytes(nbc) + L::det_bytes(nbc) + L::coef_bytes(nbc), a.aux + c0 * L::AUXW, ab,
                    &full[stage], policy);
-        if (++stage == a.stages) {
-          stage = 0;
-          phase ^= 1;
-        }
+      } else {
+        info_c0[stage] = c0;
+        info_n[stage] = -ncell;  // 0 = stop; < 0: consumers read global memory
+        mbar_arrive(&full[stage]);
+      }
+      if (++stage == a.stages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    };
+    if (a.work) {
+      // dynamic: the first a.static_batches batches are dealt round-robin,
+      // the rest are grabbed from a per-launch counter so CTAs on SMs that
+      // get more bandwidth take more of the tail.  The next grab is issued
+      // before the current batch is published, hiding the atomic's latency.
+      const int64_t n_batches = (a.n_cells + nbc - 1) / nbc;
+      for (int64_t b = blockIdx.x; b < a.static_batches; b += gridDim.x) {
+        const int64_t c0 = b * nbc;
+        publish(c0, (int)min((int64_t)nbc, a.n_cells - c0));
+      }
+      int64_t next = a.static_batches + (int64_t)atomicAdd(a.work, 1ull);
+      while (next < n_batches) {
+        const int64_t b = next;
+        next = a.static_batches + (int64_t)atomicAdd(a.work, 1ull);
+        const int64_t c0 = b * nbc;
+        publish(c0, (int)min((int64_t)nbc, a.n_cells - c0));
+      }
+    } else {
+      // static: contiguous chunks, round-robin over the CTAs
+      for (int64_t ci = blockIdx.x; ci < a.n_chunks; ci += gridDim.x) {
+        const int64_t lo = ci * a.chunk_cells;
+        const int64_t hi = min(a.n_cells, lo + a.chunk_cells);
+        for (int64_t c0 = lo; c0 < hi; c0 += nbc) publish(c0, (int)min((int64_t)nbc, hi - c0));
       }
     }
+    publish(0, 0);  // stop
     return;
   }
 
@@ -378,35 +418,46 @@ integrate_kernel(const __grid_constant__ IntegrateArgs<T> a) {
   unsigned char* scratch = scratch_base + warp * S::BYTES;
   int stage = 0;
   uint32_t phase = 0;
-  for (int64_t ci = blockIdx.x; ci < a.n_chunks; ci += gridDim.x) {
-    const int64_t lo = ci * a.chunk_cells;
-    const int64_t hi = lo + a.chunk_cells < a.n_cells ? lo + a.chunk_cells : a.n_cells;
-    for (int64_t c0 = lo; c0 < hi; c0 += nbc) {
-      const int ncell = hi - c0 < nbc ? (int)(hi - c0) : nbc;
-      T* out = a.out + c0 * NBC;
-      if (bulk_ok(ncell)) {
-        mbar_wait(&full[stage], phase);
-        const unsigned char* st = smem + stage * stage_bytes;
-        const T* s_inv = reinterpret_cast<const T*>(st);
-        const T* s_det = reinterpret_cast<const T*>(st + L::inv_bytes(nbc));
-        const T* s_coef = reinterpret_cast<const T*>(st + L::inv_bytes(nbc) + L::det_bytes(nbc));
-        const T* s_aux =
-            reinterpret_cast<const T*>(st + L::inv_bytes(nbc) + L::det_bytes(nbc) + L::coef_bytes(nbc));
-        for (int c = warp * S::CW; c < ncell; c += W * S::CW)
-          warp_slice<T, D, NQ, NCOMP, FORM, AUX, STD, true>(a.tab, s_inv, s_det, s_coef, s_aux, scratch, c,
-                                                           ncell, out, lane);
-        if (lane == 0) mbar_arrive(&empty[stage]);
-        if (++stage == a.stages) {
-          stage = 0;
-          phase ^= 1;
-        }
-      } else {
-        // unaligned caller buffers or an odd-sized last batch: read straight from global memory
-        const T* g_aux = AUX != 0 ? a.aux + c0 * L::AUXW : nullptr;
-        for (int c = warp * S::CW; c < ncell; c += W * S::CW)
-          warp_slice<T, D, NQ, NCOMP, FORM, AUX, STD, false>(a.tab, a.inv_j + c0 * DD, a.det_j + c0,
-                                                            a.coeffs + c0 * NBC, g_aux, scratch, c, ncell, out,
-                                                            lane);
+  for (;;) {
+    mbar_wait(&full[stage], phase);
+    const int64_t c0 = info_c0[stage];
+    const int nsig = info_n[stage];
+    if (nsig == 0) break;
+    T* out = a.out + c0 * NBC;
+    if (nsig > 0) {
+      const int ncell = nsig;
+      const unsigned char* st = smem + stage * stage_bytes;
+      const T* s_inv = reinterpret_cast<const T*>(st);
+      const T* s_det = reinterpret_cast<const T*>(st + L::inv_bytes(nbc));
+      const T* s_coef = reinterpret_cast<const T*>(st + L::inv_bytes(nbc) + L::det_bytes(nbc));
+      const T* s_aux = reinterpret_cast<const T*>(st + L::inv_bytes(nbc) + L::det_bytes(nbc) + L::coef_bytes(nbc));
+      for (int c = warp * S::CW; c < ncell; c += W * S::CW)
+        warp_slice<T, D, NQ, NCOMP, FORM, AUX, STD, true>(a.tab, s_inv, s_det, s_coef, s_aux, scratch, c, ncell,
+                                                         out, lane);
+    } else {
+      // unaligned caller buffers or an odd-sized partial batch: straight from global memory
+      const int ncell = -nsig;
+      const T* g_aux = AUX != 0 ? a.aux + c0 * L::AUXW : nullptr;
+      for (int c = warp * S::CW; c < ncell; c += W * S::CW)
+        warp_slice<T, D, NQ, NCOMP, FORM, AUX, STD, false>(a.tab, a.inv_j + c0 * DD, a.det_j + c0,
+                                                          a.coeffs + c0 * NBC, g_aux, scratch, c, ncell, out,
+                                                          lane);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == a.stages) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+  // dynamic mode: the last CTA out resets the per-launch counters for the
+  // next launch that draws this slot (stream order / PDL wait make it visible)
+  if (a.work && lane == 0) {
+    if (atomicAdd(&warps_done, 1) == W - 1) {
+      __threadfence();
+      if (atomicAdd(a.work + 1, 1ull) == (unsigned long long)gridDim.x - 1) {
+        atomicExch(a.work, 0ull);
+        atomicExch(a.work + 1, 0ull);
       }
     }
   }
@@ -423,6 +474,7 @@ struct Config {
 struct Geometry {
   int n_bl, n_cb, n_bc, n_t, threads, warps, stages, smem, grid;
   int64_t n_chunks, chunk_cells;
+  bool dynamic;
 };
 
 static int env_int(const char* name, int dflt) {
@@ -602,7 +654,7 @@ static int compute_geometry(const Config& c, const KernelInfo& k, int64_t n_cell
   g.threads = 32 * (g.warps + 1);
 
   const int stage = k.stage_bytes(g.n_bc);
-  const int fixed = g.warps * k.scratch(g.n_bc) + 16 * 8;  // scratch + 2*8 mbarriers
+  const int fixed = g.warps * k.scratch(g.n_bc) + 256;  // scratch + mbarriers + stage info
   int smem_cap = 227 * 1024;
   int dev = 0, sms = 148;
   if (query_device && cudaGetDevice(&dev) == cudaSuccess) {
@@ -695,7 +747,37 @@ static int compute_geometry(const Config& c, const KernelInfo& k, int64_t n_cell
   }
   g.n_chunks = (n_cells + g.chunk_cells - 1) / g.chunk_cells;
   g.grid = (int)std::max<int64_t>(1, std::min<int64_t>(g.n_chunks, resident));
+  // Default: dynamic batch scheduling (a per-launch atomic counter) so CTAs on
+  // SMs that get more bandwidth take more batches and all finish together.
+  // An explicit n_cb keeps the paper's static chunk order.
+  // Only worth it when a batch is long enough to hide the counter's atomic
+  // latency (>= 10 KB per stage; measured, profiles/r1_sweep.md).
+  const int dyn_env = env_int("TXB_DYNAMIC", -1);
+  g.dynamic = n_cb <= 0 && (dyn_env < 0 ? stage >= 10 * 1024 : dyn_env != 0);
+  if (g.dynamic) {
+    const int64_t n_batches = (n_cells + g.n_bc - 1) / g.n_bc;
+    g.grid = (int)std::max<int64_t>(1, std::min<int64_t>(n_batches, resident));
+  }
   return TXB_OK;
+}
+
+// Device address of the dynamic-scheduling counter pool on the current device.
+static unsigned long long* work_pool_base() {
+  static std::mutex mu;
+  static std::vector<unsigned long long*> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if ((int)cache.size() <= dev) cache.resize(dev + 1, nullptr);
+  if (!cache[dev]) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, g_work_pool) != cudaSuccess) {
+      cuda_fail(cudaGetLastError(), "cudaGetSymbolAddress(g_work_pool)");
+      return nullptr;
+    }
+    cache[dev] = (unsigned long long*)p;
+  }
+  return cache[dev];
 }
 
 template <typename T>
@@ -723,6 +805,19 @@ static int launch_t(const Config& c, const KernelInfo& k, const Geometry& g, int
   a.n_bc = g.n_bc;
   a.stages = g.stages;
   a.warps = g.warps;
+  a.work = nullptr;
+  if (g.dynamic) {
+    unsigned long long* pool = work_pool_base();
+    if (!pool) return TXB_E_CUDA;
+    static std::atomic<uint64_t> seq{0};
+    a.work = pool + 2 * (seq.fetch_add(1) % WORK_POOL);
+    // deal ~TXB_STATIC_PCT % of the batches statically (whole rounds of the grid)
+    const int64_t n_batches = (n_cells + g.n_bc - 1) / g.n_bc;
+    const int pct = std::min(100, std::max(0, env_int("TXB_STATIC_PCT", 60)));
+    a.static_batches = n_batches * pct / 100 / g.grid * g.grid;
+  } else {
+    a.static_batches = 0;
+  }
   // Bulk copies need 16-byte aligned, 16-byte sized slices for EVERY batch:
   // aligned base pointers and N_bc * (per-cell scalars) * sizeof(T) % 16 == 0
   // for each of the four arrays.  Otherwise every batch is read from global.

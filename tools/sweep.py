@@ -25,13 +25,16 @@ def main():
         wl = bench.rank_workload(name, 0, 1)
         n_sets = max(4, -(-3 * bench.L2_BYTES // (bpc * wl["n"])) + 1)
         best = None
-        grid = [(c, sm, st, pdl) for c in (64, 128, 256) for sm in (40, 56, 80, 110) for st in (0,)
-                for pdl in (0, 1)]
-        for threads, smem, stages, pdl in grid:
+        knobs = os.environ.get("SWEEP_GRID", "cells=128,256 inflight=48,72 dyn=0,1 pct=50,75,90")
+        kv = dict(x.split("=") for x in knobs.split())
+        grid = [(int(c), int(i), int(dy), int(pc)) for c in kv["cells"].split(",")
+                for i in kv["inflight"].split(",") for dy in kv["dyn"].split(",")
+                for pc in (kv["pct"].split(",") if dy == "1" else ["0"])]
+        for threads, smem, pdl, pct in grid:
+            os.environ["TXB_STATIC_PCT"] = str(pct)
             os.environ["TXB_TARGET_CELLS"] = str(threads)
-            os.environ["TXB_SMEM_TARGET"] = str(smem * 1024)
-            os.environ["TXB_STAGES"] = str(stages)
-            os.environ["TXB_PDL"] = str(pdl)
+            os.environ["TXB_INFLIGHT_KB"] = str(smem)
+            os.environ["TXB_DYNAMIC"] = str(pdl)
             try:
                 tot, _ = bench.time_device(wl, 200, 5, n_sets)
             except Exception as exc:  # capacity etc.
@@ -45,13 +48,13 @@ def main():
             w = 4 if wl["dtype"] == "f32" else 8
             cfg = backend.launch_config(*backend.cuda_kernel(form, 1, wl["aux"], w), w, wl["dim"], 1,
                                         form.n_comp, wl["n"])
-            rec = {"config": name, "cells": threads, "smem_kb": smem, "pdl": pdl, "gbs": round(gbs, 1),
+            rec = {"config": name, "cells": threads, "inflight_kb": smem, "dynamic": pdl, "static_pct": pct, "gbs": round(gbs, 1),
                    "frac": round(gbs / peak, 3), "us": round(ms * 1e3, 2), **cfg}
             print(json.dumps(rec), flush=True)
             if best is None or gbs > best["gbs"]:
                 best = rec
         print("BEST", json.dumps(best), flush=True)
-        for k in ("TXB_TARGET_CELLS", "TXB_SMEM_TARGET", "TXB_STAGES", "TXB_PDL"):
+        for k in ("TXB_TARGET_CELLS", "TXB_INFLIGHT_KB", "TXB_DYNAMIC", "TXB_STATIC_PCT"):
             os.environ.pop(k, None)
         del wl
         torch.cuda.empty_cache()

@@ -13,6 +13,8 @@
  *                             and txfem/executor.py:109-114 _run_span(...)
  *   txb_integrate_cells_host  same call with HOST buffers (the reference's own
  *                             calling convention: numpy arrays in host memory)
+ *   txb_integrate_mesh     <- txfem/executor.py:194-212 (geometry + gather + cast
+ *                             + integrate_cells, fused into one kernel)
  *   txb_gather_coefficients   <- txfem/mesh.py:202-217 gather_coefficients
  *   txb_scatter_add           <- txfem/mesh.py:220-234 scatter_add_element_vectors
  *   txb_compute_geometry      <- txfem/mesh.py:150-190 compute_geometry
@@ -108,6 +110,27 @@ int txb_integrate_cells_host(int form_code, int aux_mode, int dtype_bytes, int d
                              const void* basis, const void* basis_der, const void* weights,
                              const void* inv_j, const void* det_j, const void* coeffs,
                              const void* aux, void* out, int n_bl, int n_cb);
+
+/* Element integration fused with the reference's host-side preparation
+ * (txfem/executor.py:194-212: compute_geometry, gather_coefficients, cast):
+ * per-cell element vectors straight from the mesh.  DEVICE pointers:
+ *   vertices (n_vertices, dim) float64, cells int64 (n_cells, dim+1),
+ *   coeffs_global (n_vertices * n_comp) in the run dtype, aux per cell as in
+ *   txb_integrate_cells, out (n_cells, dim+1, n_comp).
+ * inv_j / det_j: NULL to compute the geometry from the vertices (float64,
+ * mesh.py:150-190 expression order, then cast), or the caller's geometry in
+ * the run dtype.  bad_cell: NULL or a device int64 preset to -1 (all bits
+ * set); lowered to the first cell with detJ <= 0 (OrientationError).
+ * Needs the standard P1 tabulation with n_q <= 2 (TXB_E_UNSUPPORTED
+ * otherwise: use the unfused entry points).  Bit-identical to
+ * compute_geometry -> gather -> cast -> txb_integrate_cells.  n_bl <= 0:
+ * tuned default.  Asynchronous on `stream`. */
+int txb_integrate_mesh(int form_code, int aux_mode, int dtype_bytes, int dim, int n_q, int n_comp,
+                       int64_t n_cells, int64_t n_vertices,
+                       const void* basis, const void* basis_der, const void* weights,
+                       const double* vertices, const int64_t* cells, const void* coeffs_global,
+                       const void* inv_j, const void* det_j, const void* aux, void* out,
+                       int64_t* bad_cell, int n_bl, void* stream);
 
 /* Gather per-cell coefficient blocks (device pointers):
  *   out[c][b][k] = global[cells[c][b] * n_comp + k],  cells int64 (n, n_b). */

@@ -31,6 +31,7 @@ SIGNATURES = {
     "txb_launch_config": (_I, [_I, _I, _I, _I, _I, _I, c_int64, _I, _I] + [POINTER(c_int)] * 7),
     "txb_integrate_cells": (_I, [_I, _I, _I, _I, _I, _I, _I, c_int64] + [_P] * 8 + [_I, _I, _P]),
     "txb_integrate_cells_host": (_I, [_I, _I, _I, _I, _I, _I, _I, c_int64] + [_P] * 8 + [_I, _I]),
+    "txb_integrate_mesh": (_I, [_I, _I, _I, _I, _I, _I, c_int64, c_int64] + [_P] * 11 + [_I, _P]),
     "txb_gather_coefficients": (_I, [_I, c_int64, _I, _I, _P, _P, _P, _P]),
     "txb_scatter_add": (_I, [_I, c_int64, _I, _P, _P, _P, _P, _P]),
     "txb_incidence_scratch_bytes": (c_int64, [c_int64, _I, c_int64]),

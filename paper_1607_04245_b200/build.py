@@ -16,8 +16,8 @@ PKG = Path(__file__).resolve().parent
 REPO = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libtxb.so"
-SOURCES = [CSRC / "txb_integrate.cu", CSRC / "txb_mesh.cu"]
-HEADERS = [CSRC / "txb_common.cuh", REPO / "include" / "txb.h"]
+SOURCES = [CSRC / "txb_integrate.cu", CSRC / "txb_integrate_mesh.cu", CSRC / "txb_mesh.cu"]
+HEADERS = [CSRC / "txb_common.cuh", CSRC / "txb_kernels.cuh", REPO / "include" / "txb.h"]
 
 NVCC_FLAGS = [
     "-std=c++17", "-O3", "-lineinfo",
@@ -37,12 +37,26 @@ def _stale(target: Path, deps) -> bool:
 
 
 def build_library(force: bool = False, verbose: bool = False) -> Path:
+    """Compile each translation unit in parallel (they share no device code),
+    then link the shared library."""
     if force or _stale(LIB, SOURCES + HEADERS):
         nvcc = os.environ.get("NVCC", "nvcc")
-        cmd = [nvcc, *NVCC_FLAGS, f"-I{REPO / 'include'}", "-o", str(LIB), *map(str, SOURCES)]
-        if verbose:
-            cmd.insert(1, "-Xptxas=-v")
-        subprocess.run(cmd, check=True)
+        objdir = PKG / "build_obj"
+        objdir.mkdir(exist_ok=True)
+        procs = []
+        for src in SOURCES:
+            obj = objdir / (src.stem + ".o")
+            cmd = [nvcc, *[f for f in NVCC_FLAGS if f != "-shared"], f"-I{REPO / 'include'}", "-c", "-o", str(obj),
+                   str(src)]
+            if verbose:
+                cmd.insert(1, "-Xptxas=-v")
+            procs.append((subprocess.Popen(cmd), cmd))
+        for p, cmd in procs:
+            if p.wait() != 0:
+                raise subprocess.CalledProcessError(p.returncode, cmd)
+        objs = [str(objdir / (s.stem + ".o")) for s in SOURCES]
+        subprocess.run([nvcc, "-shared", "-cudart", "static", "-gencode", "arch=compute_100a,code=sm_100a",
+                        "-o", str(LIB), *objs], check=True)
     return LIB
 
 

@@ -95,4 +95,42 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __host__ __device__ constexpr int round_up(int x, int m) { return (x + m - 1) / m * m; }
 __host__ __device__ constexpr int make_odd(int x) { return (x & 1) ? x : x + 1; }
 
+// ---------------------------------------------------------------------------
+// Affine map inverse of a simplex, float64, in the reference's expression
+// order (txfem/mesh.py:150-190): J's column k = v_{k+1} - v_0; 2D closed form,
+// 3D cofactors; numpy evaluates a*b - c*d as two rounded products and one
+// rounded difference and sums the 3x3 determinant left to right.  Every
+// operation is an _rn intrinsic, so the result is bit-identical to numpy.
+// ---------------------------------------------------------------------------
+template <int D>
+__device__ __forceinline__ void affine_inverse(const double (&X)[D + 1][D], double (&inv)[D * D], double& det) {
+  double m[D][D];
+#pragma unroll
+  for (int k = 0; k < D; ++k)
+#pragma unroll
+    for (int i = 0; i < D; ++i) m[i][k] = __dsub_rn(X[k + 1][i], X[0][i]);
+  if constexpr (D == 2) {
+    const double a = m[0][0], b = m[0][1], c = m[1][0], e = m[1][1];
+    det = __dsub_rn(__dmul_rn(a, e), __dmul_rn(b, c));
+    inv[0] = __ddiv_rn(e, det);
+    inv[1] = __ddiv_rn(-b, det);
+    inv[2] = __ddiv_rn(-c, det);
+    inv[3] = __ddiv_rn(a, det);
+  } else {
+    const double cof00 = __dsub_rn(__dmul_rn(m[1][1], m[2][2]), __dmul_rn(m[1][2], m[2][1]));
+    const double cof01 = __dsub_rn(__dmul_rn(m[1][2], m[2][0]), __dmul_rn(m[1][0], m[2][2]));
+    const double cof02 = __dsub_rn(__dmul_rn(m[1][0], m[2][1]), __dmul_rn(m[1][1], m[2][0]));
+    det = __dadd_rn(__dadd_rn(__dmul_rn(m[0][0], cof00), __dmul_rn(m[0][1], cof01)), __dmul_rn(m[0][2], cof02));
+    inv[0 * 3 + 0] = __ddiv_rn(cof00, det);
+    inv[1 * 3 + 0] = __ddiv_rn(cof01, det);
+    inv[2 * 3 + 0] = __ddiv_rn(cof02, det);
+    inv[0 * 3 + 1] = __ddiv_rn(__dsub_rn(__dmul_rn(m[0][2], m[2][1]), __dmul_rn(m[0][1], m[2][2])), det);
+    inv[1 * 3 + 1] = __ddiv_rn(__dsub_rn(__dmul_rn(m[0][0], m[2][2]), __dmul_rn(m[0][2], m[2][0])), det);
+    inv[2 * 3 + 1] = __ddiv_rn(__dsub_rn(__dmul_rn(m[0][1], m[2][0]), __dmul_rn(m[0][0], m[2][1])), det);
+    inv[0 * 3 + 2] = __ddiv_rn(__dsub_rn(__dmul_rn(m[0][1], m[1][2]), __dmul_rn(m[0][2], m[1][1])), det);
+    inv[1 * 3 + 2] = __ddiv_rn(__dsub_rn(__dmul_rn(m[0][2], m[1][0]), __dmul_rn(m[0][0], m[1][2])), det);
+    inv[2 * 3 + 2] = __ddiv_rn(__dsub_rn(__dmul_rn(m[0][0], m[1][1]), __dmul_rn(m[0][1], m[1][0])), det);
+  }
+}
+
 }  // namespace txb

@@ -1,0 +1,517 @@
+// txb_kernels.cuh — device and host building blocks shared by the streaming
+// kernels (cell-array integration, mesh-fused integration): tabulation in the
+// parameter space, ring-stage layouts, the warp-specialised bulk-copy batch
+// pipeline, launch-geometry selection.  See txb_integrate.cu for the design.
+#pragma once
+
+#include "txb_common.cuh"
+
+#include <algorithm>
+#include <atomic>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
+namespace txb {
+
+constexpr int MAX_D = TXB_MAX_DIM, MAX_B = TXB_MAX_BASIS, MAX_Q = TXB_MAX_QUAD;
+constexpr int MAX_CONSUMER_WARPS = 16;
+constexpr int MAX_STAGES = 8;
+constexpr int WORK_POOL = 4096;  // per-launch dynamic-scheduling counters (device globals, zero at load)
+// one pool per translation unit (static): each kernel family draws its own slots
+static __device__ unsigned long long g_work_pool[WORK_POOL][2];
+constexpr int MAX_CTA_THREADS = 32 * (MAX_CONSUMER_WARPS + 1);
+
+template <typename T>
+struct Tabulation {
+  T B[MAX_Q * MAX_B];          // basis[q][b]
+  T D[MAX_Q * MAX_B * MAX_D];  // basis_der[q][b][j]
+  T W[MAX_Q];                  // weights[q]
+};
+
+// Byte layout of one ring stage: four 16-byte aligned regions holding the
+// batch's contiguous slices of inv_j, det_j, coeffs and aux.
+template <typename T, int D, int NCOMP, int AUX>
+struct StageLayout {
+  static constexpr int NB = D + 1;
+  static constexpr int AUXW = AUX == 1 ? 1 : (AUX == 2 ? NB : 0);
+  __host__ __device__ static int inv_bytes(int n) { return round_up(n * D * D * (int)sizeof(T), 16); }
+  __host__ __device__ static int det_bytes(int n) { return round_up(n * (int)sizeof(T), 16); }
+  __host__ __device__ static int coef_bytes(int n) { return round_up(n * NB * NCOMP * (int)sizeof(T), 16); }
+  __host__ __device__ static int aux_bytes(int n) { return round_up(n * AUXW * (int)sizeof(T), 16); }
+  __host__ __device__ static int stage_bytes(int n) {
+    return inv_bytes(n) + det_bytes(n) + coef_bytes(n) + aux_bytes(n);
+  }
+};
+
+// Warp-private exchange area between the two phases.  STD (standard P1
+// tables): only T[0][k] is stored (the other rows are invJ rows, read from the
+// stage); otherwise all T[q][b][k].  T strides are odd (bank-conflict free
+// scalar access); the f1 rows are padded to 16 bytes so the basis phase reads
+// them with vector loads (a warp touches 32/(N_b N_comp) cells per access).
+template <typename T, int D, int NQ, int NCOMP, bool STD>
+struct Scratch {
+  static constexpr int NB = D + 1;
+  static constexpr int CW = 32 / NQ;  // cells per warp slice
+  static constexpr int TR = STD ? D : NQ * NB * D;
+  static constexpr int F1 = NQ * NCOMP * D;
+  static constexpr int VEC = 16 / (int)sizeof(T);
+  static constexpr int TRS = make_odd(TR);
+  static constexpr int F1S = NCOMP == 1 ? round_up(F1, VEC) : make_odd(F1);
+  static constexpr int TR_BYTES = round_up(CW * TRS * (int)sizeof(T), 16);
+  static constexpr int BYTES = TR_BYTES + CW * F1S * (int)sizeof(T);
+};
+
+// Vectorised row load: N consecutive T at p (row starts are multiples of
+// N*sizeof(T) from a 16-byte aligned base); widest access the alignment allows.
+template <typename T, int N, bool VEC = true>
+__device__ __forceinline__ void load_row(const T* __restrict__ p, T (&r)[N]) {
+  constexpr int BYTES = N * (int)sizeof(T);
+  if constexpr (!VEC) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) r[i] = p[i];
+  } else if constexpr (BYTES % 16 == 0) {
+    constexpr int V = 16 / sizeof(T);
+#pragma unroll
+    for (int i = 0; i < N; i += V) {
+      const uint4 v = *reinterpret_cast<const uint4*>(p + i);
+      memcpy(&r[i], &v, 16);
+    }
+  } else if constexpr (BYTES % 8 == 0) {
+    constexpr int V = 8 / sizeof(T);
+#pragma unroll
+    for (int i = 0; i < N; i += V) {
+      const uint2 v = *reinterpret_cast<const uint2*>(p + i);
+      memcpy(&r[i], &v, 8);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) r[i] = p[i];
+  }
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Exactness note (why the chains below may skip the reference's "acc = 0;
+// acc = acc + x" first step and its 0*x / 1*x products): in round-to-nearest
+// a sum is -0 only if both operands are -0, so a chain started at +0 is never
+// -0, and chains started at +0 vs at their first term differ at most in the
+// SIGN OF A ZERO.  Every intermediate (T, grad u, f1s) only ever enters
+// products that are summed into such a +0-started chain, where a zero term of
+// either sign leaves the partial sum unchanged.  Hence only the final
+// element-vector chain must start at +0 to reproduce the reference bit for
+// bit; everything upstream may drop exact no-ops.  (Finite inputs.)
+
+// ---------------------------------------------------------------------------
+// The batch pipeline shared by every streaming kernel of the library.
+//
+// Args provides: n_cells, n_chunks, chunk_cells, n_bc, stages, warps, work,
+// static_batches.  One producer lane (warp `warps`, lane 0) walks the batch
+// sequence -- static contiguous chunks, or round-robin + a per-launch atomic
+// counter for the tail (`work` != NULL) -- and for each batch calls
+//     issue(stage_ptr, c0, ncell, full_bar)  -> true if it posted expect_tx and
+//                                              bulk copies, false if the batch
+//                                              must be read from global memory
+// Consumer warps wait on the stage's `full` barrier and call
+//     consume(stage_ptr or nullptr, c0, ncell)
+// then arrive on `empty`.  A count of 0 published in the stage info stops them.
+// ---------------------------------------------------------------------------
+struct PipelineSmem {
+  uint64_t* full;
+  uint64_t* empty;
+  int64_t* info_c0;
+  int* info_n;
+  int* warps_done;
+};
+
+// mbarriers + stage info + done counter, carved after `base`
+__device__ __forceinline__ PipelineSmem carve_pipeline(unsigned char* base) {
+  PipelineSmem p;
+  p.full = reinterpret_cast<uint64_t*>(base);
+  p.empty = p.full + MAX_STAGES;
+  p.info_c0 = reinterpret_cast<int64_t*>(p.empty + MAX_STAGES);
+  p.info_n = reinterpret_cast<int*>(p.info_c0 + MAX_STAGES);
+  p.warps_done = p.info_n + MAX_STAGES;
+  return p;
+}
+constexpr int PIPELINE_SMEM_BYTES = 8 * (3 * MAX_STAGES) + 4 * MAX_STAGES + 16;
+
+template <class Args>
+__device__ __forceinline__ void pipeline_init(const Args& a, const PipelineSmem& p) {
+  if (threadIdx.x == 0) {
+    *p.warps_done = 0;
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(&p.full[s], 1);
+      mbar_init(&p.empty[s], a.warps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  // Programmatic dependent launch: everything above overlapped the previous
+  // grid in the stream; from here on we touch global memory, so wait for it
+  // (no-op when launched without the PDL attribute), then let the next grid
+  // start its own prologue as our CTAs retire.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <class Args, class Issue>
+__device__ __forceinline__ void pipeline_produce(const Args& a, const PipelineSmem& p, unsigned char* stages,
+                                                 int stage_bytes, Issue issue) {
+  const int nbc = a.n_bc;
+  int stage = 0;
+  uint32_t phase = 0;
+  auto publish = [&](int64_t c0, int ncell) {
+    mbar_wait(&p.empty[stage], phase ^ 1);
+    p.info_c0[stage] = c0;
+    p.info_n[stage] = ncell;  // 0 = stop
+    if (ncell == 0 || !issue(stages + stage * stage_bytes, c0, ncell, &p.full[stage])) {
+      if (ncell) p.info_n[stage] = -ncell;  // consumers read this batch from global memory
+      mbar_arrive(&p.full[stage]);
+    }
+    if (++stage == a.stages) {
+      stage = 0;
+      phase ^= 1;
+    }
+  };
+  if (a.work) {
+    // dynamic: the first a.static_batches batches are dealt round-robin,
+    // the rest are grabbed from a per-launch counter so CTAs on SMs that
+    // get more bandwidth take more of the tail.  The next grab is issued
+    // before the current batch is published, hiding the atomic's latency.
+    const int64_t n_batches = (a.n_cells + nbc - 1) / nbc;
+    for (int64_t b = blockIdx.x; b < a.static_batches; b += gridDim.x) {
+      const int64_t c0 = b * nbc;
+      publish(c0, (int)min((int64_t)nbc, a.n_cells - c0));
+    }
+    int64_t next = a.static_batches + (int64_t)atomicAdd(a.work, 1ull);
+    while (next < n_batches) {
+      const int64_t b = next;
+      next = a.static_batches + (int64_t)atomicAdd(a.work, 1ull);
+      const int64_t c0 = b * nbc;
+      publish(c0, (int)min((int64_t)nbc, a.n_cells - c0));
+    }
+  } else {
+    // static: contiguous chunks, round-robin over the CTAs
+    for (int64_t ci = blockIdx.x; ci < a.n_chunks; ci += gridDim.x) {
+      const int64_t lo = ci * a.chunk_cells;
+      const int64_t hi = min(a.n_cells, lo + a.chunk_cells);
+      for (int64_t c0 = lo; c0 < hi; c0 += nbc) publish(c0, (int)min((int64_t)nbc, hi - c0));
+    }
+  }
+  publish(0, 0);  // stop
+}
+
+template <class Args, class Consume>
+__device__ __forceinline__ void pipeline_consume(const Args& a, const PipelineSmem& p, unsigned char* stages,
+                                                 int stage_bytes, Consume consume) {
+  const int lane = threadIdx.x & 31;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (;;) {
+    mbar_wait(&p.full[stage], phase);
+    const int64_t c0 = p.info_c0[stage];
+    const int nsig = p.info_n[stage];
+    if (nsig == 0) break;
+    if (nsig > 0)
+      consume(stages + stage * stage_bytes, c0, nsig);
+    else
+      consume(nullptr, c0, -nsig);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&p.empty[stage]);
+    if (++stage == a.stages) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+  // dynamic mode: the last CTA out resets the per-launch counters for the
+  // next launch that draws this slot (stream order / PDL wait make it visible)
+  if (a.work && lane == 0) {
+    if (atomicAdd(p.warps_done, 1) == a.warps - 1) {
+      __threadfence();
+      if (atomicAdd(a.work + 1, 1ull) == (unsigned long long)gridDim.x - 1) {
+        atomicExch(a.work, 0ull);
+        atomicExch(a.work + 1, 0ull);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host-side launch geometry (shared)
+// ---------------------------------------------------------------------------
+struct Config {
+  int form, aux, dtype, dim, n_q, n_comp;
+};
+
+struct Geometry {
+  int n_bl, n_cb, n_bc, n_t, threads, warps, stages, smem, grid;
+  int64_t n_chunks, chunk_cells;
+  bool dynamic;
+};
+
+static int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return (v && *v) ? std::atoi(v) : dflt;
+}
+
+static int validate(const Config& c) {
+  if (c.dtype != 4 && c.dtype != 8) {
+    set_error("dtype_bytes must be 4 or 8, got %d", c.dtype);
+    return TXB_E_UNSUPPORTED;
+  }
+  if (c.dim < 2 || c.dim > 3) {
+    set_error("dim must be 2 or 3, got %d", c.dim);
+    return TXB_E_UNSUPPORTED;
+  }
+  if (c.n_q < 1 || c.n_q > MAX_Q) {
+    set_error("n_q must be in [1, %d], got %d", MAX_Q, c.n_q);
+    return TXB_E_UNSUPPORTED;
+  }
+  const bool ok = (c.form == 0 && c.aux == 0 && c.n_comp == 1) ||
+                  (c.form == 1 && (c.aux == 1 || c.aux == 2) && c.n_comp == 1) ||
+                  (c.form == 2 && c.aux == 0 && c.n_comp == c.dim);
+  if (!ok) {
+    set_error("cuda lane does not cover form_code=%d aux_mode=%d n_comp=%d dim=%d", c.form, c.aux, c.n_comp,
+              c.dim);
+    return TXB_E_UNSUPPORTED;
+  }
+  return TXB_OK;
+}
+
+static int gcd(int a, int b) { return b ? gcd(b, a % b) : a; }
+
+// Default N_bl: batch near TXB_TARGET_CELLS (256) cells, N_bc a multiple of
+// the warp slice CW = 32/N_q so no warp slice is partial.
+static void default_decomposition(const Config& c, int& n_bl, int& n_cb) {
+  const int nbs = (c.dim + 1) * c.n_q;
+  if (n_bl <= 0) {
+    const int cw = 32 / c.n_q;
+    const int step = cw / gcd(cw, nbs);  // n_bl multiple of step -> N_bc multiple of cw
+    const int target = env_int("TXB_TARGET_CELLS", c.dtype == 8 ? 128 : 256);
+    int best = step, best_err = 1 << 30;
+    for (int m = 1; m * step * nbs <= 1024; ++m) {
+      const int err = std::abs(m * step * nbs - target);
+      if (err < best_err) {
+        best_err = err;
+        best = m * step;
+      }
+    }
+    n_bl = best;
+  }
+  if (n_cb <= 0) n_cb = env_int("TXB_DEFAULT_NCB", 0);  // 0: balanced contiguous chunks
+}
+
+struct KernelInfo {
+  void* fn;
+  int (*stage_bytes)(int);
+  int (*scratch)(int);  // per consumer warp
+  int cw;
+};
+
+// True when every tabulated reference gradient is exactly the P1 one:
+// D[q][0][j] = -1, D[q][b][j] = (b-1 == j) for b >= 1 (element.py:55-77).
+template <typename T>
+static bool is_standard_p1(const void* basis_der, int n_q, int d) {
+  const T* D = (const T*)basis_der;
+  const int nb = d + 1;
+  for (int q = 0; q < n_q; ++q)
+    for (int b = 0; b < nb; ++b)
+      for (int j = 0; j < d; ++j) {
+        const T want = b == 0 ? T(-1) : (b - 1 == j ? T(1) : T(0));
+        const T got = D[(q * nb + b) * d + j];
+        if (memcmp(&got, &want, sizeof(T)) != 0) return false;  // bitwise (no -0)
+      }
+  return true;
+}
+
+static bool standard_tables(const Config& c, const void* basis_der) {
+  if (!basis_der) return false;
+  return c.dtype == 4 ? is_standard_p1<float>(basis_der, c.n_q, c.dim)
+                      : is_standard_p1<double>(basis_der, c.n_q, c.dim);
+}
+
+struct DeviceProps {
+  int sms = 0, smem_optin = 0;
+};
+
+static DeviceProps device_props(int dev) {
+  static std::mutex mu;
+  static std::vector<DeviceProps> cache;
+  std::lock_guard<std::mutex> g(mu);
+  if ((int)cache.size() <= dev) cache.resize(dev + 1);
+  if (cache[dev].sms == 0) {
+    cudaDeviceGetAttribute(&cache[dev].sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&cache[dev].smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  }
+  return cache[dev];
+}
+
+static int compute_geometry(const Config& c, const KernelInfo& k, int64_t n_cells, int n_bl, int n_cb,
+                            bool query_device, Geometry& g) {
+  default_decomposition(c, n_bl, n_cb);
+  const int nb = c.dim + 1;
+  const int64_t n_bc64 = (int64_t)n_bl * nb * c.n_q;
+  const int64_t n_t64 = n_bc64 * c.n_comp;
+  if (n_bl < 1 || n_cb < 0) {
+    set_error("n_bl must be >= 1 and n_cb >= 1 (got %d, %d)", n_bl, n_cb);
+    return TXB_E_CONFIG;
+  }
+  if (n_t64 > TXB_THREAD_LIMIT) {
+    // txfem/schedule.py:86-90: the paper's thread block may not exceed the device limit.
+    set_error("thread block needs %lld threads, device limit is %d (n_bs=%d * n_comp=%d * n_bl=%d)",
+              (long long)n_t64, TXB_THREAD_LIMIT, nb * c.n_q, c.n_comp, n_bl);
+    return TXB_E_CONFIG;
+  }
+  g.n_bl = n_bl;
+  g.n_cb = n_cb;
+  g.n_bc = (int)n_bc64;
+  g.n_t = (int)n_t64;
+  const int slices = (g.n_bc + k.cw - 1) / k.cw;
+  const int wcap = std::max(1, std::min(MAX_CONSUMER_WARPS, env_int("TXB_MAX_WARPS", MAX_CONSUMER_WARPS)));
+  g.warps = std::min(wcap, slices);
+  g.threads = 32 * (g.warps + 1);
+
+  const int stage = k.stage_bytes(g.n_bc);
+  const int fixed = g.warps * k.scratch(g.n_bc) + PIPELINE_SMEM_BYTES + 16;
+  int smem_cap = 227 * 1024;
+  int dev = 0, sms = 148;
+  if (query_device && cudaGetDevice(&dev) == cudaSuccess) {
+    DeviceProps p = device_props(dev);
+    if (p.smem_optin > 0) smem_cap = p.smem_optin;
+    if (p.sms > 0) sms = p.sms;
+  }
+  // Ring depth: keep about TXB_INFLIGHT_KB (72 KB) of batch loads in flight
+  // per SM -- (CTAs/SM) x (stages-1) x stage bytes ~ HBM bandwidth x latency
+  // per SM.  Deeper rings only queue more requests and lengthen the launch
+  // ramp (measured, profiles/r1_sweep.md).  TXB_STAGES forces a depth.
+  const int forced = env_int("TXB_STAGES", 0);
+  const int64_t inflight_target = (int64_t)env_int("TXB_INFLIGHT_KB", 72) * 1024;
+  auto occupancy = [&](int smem) {
+    int occ = 1;
+    if (query_device) {
+      static std::mutex mu;
+      std::lock_guard<std::mutex> lk(mu);
+      cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.fn, g.threads, smem) != cudaSuccess || occ < 1)
+        occ = 1;
+    } else {
+      occ = std::max(1, std::min(2048 / g.threads, smem_cap / std::max(smem, 1)));
+    }
+    return occ;
+  };
+  int best_s = -1, occ = 1;
+  int64_t best_err = -1;
+  // the choice depends only on the kernel shape: memoise it (the occupancy
+  // queries cost microseconds of host time per launch otherwise)
+  struct Key {
+    void* fn;
+    int threads, stage, fixed, forced, dev;
+    int64_t target;
+    bool operator<(const Key& o) const {
+      return std::tie(fn, threads, stage, fixed, forced, dev, target) <
+             std::tie(o.fn, o.threads, o.stage, o.fixed, o.forced, o.dev, o.target);
+    }
+  };
+  static std::mutex memo_mu;
+  static std::map<Key, std::pair<int, int>> memo;
+  const Key key{k.fn, g.threads, stage, fixed, forced, query_device ? dev : -1, inflight_target};
+  {
+    std::lock_guard<std::mutex> lk(memo_mu);
+    auto it = memo.find(key);
+    if (it != memo.end()) {
+      best_s = it->second.first;
+      occ = it->second.second;
+    }
+  }
+  const bool memoised = best_s >= 0;
+  for (int st = 2; !memoised && st <= 8; ++st) {
+    if (forced > 0 && st != std::min(std::max(forced, 2), 8)) continue;
+    const int smem = fixed + st * stage;
+    if (smem > smem_cap) break;
+    const int o = occupancy(smem);
+    const int64_t err = std::llabs((int64_t)o * (st - 1) * stage - inflight_target);
+    if (best_s < 0 || err < best_err) {
+      best_s = st;
+      best_err = err;
+      occ = o;
+    }
+  }
+  if (best_s < 0) {
+    set_error("shared-memory image needs %d bytes, budget is %d (n_bl=%d, scalar width %d)", fixed + 2 * stage,
+              smem_cap, n_bl, c.dtype);
+    return TXB_E_CAPACITY;
+  }
+  if (!memoised) {
+    std::lock_guard<std::mutex> lk(memo_mu);
+    memo[key] = {best_s, occ};
+  }
+  g.stages = best_s;
+  g.smem = fixed + best_s * stage;
+  if (query_device) {
+    static std::mutex mu2;
+    std::lock_guard<std::mutex> lk(mu2);
+    cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem);
+  }
+  const int64_t resident = (int64_t)occ * sms;
+  if (n_cb > 0) {
+    // paper mode: chunks of N_cb batches, round-robin over the CTAs
+    g.chunk_cells = (int64_t)n_cb * g.n_bc;
+  } else {
+    // balanced mode: one contiguous chunk per resident CTA, 16-cell granular
+    // (keeps every bulk-copy slice 16-byte aligned), so all CTAs finish together
+    const int64_t per = (n_cells + resident - 1) / std::max<int64_t>(resident, 1);
+    g.chunk_cells = std::max<int64_t>(16, (per + 15) / 16 * 16);
+    g.n_cb = (int)((g.chunk_cells + g.n_bc - 1) / g.n_bc);
+  }
+  g.n_chunks = (n_cells + g.chunk_cells - 1) / g.chunk_cells;
+  g.grid = (int)std::max<int64_t>(1, std::min<int64_t>(g.n_chunks, resident));
+  // Default: dynamic batch scheduling (a per-launch atomic counter) so CTAs on
+  // SMs that get more bandwidth take more batches and all finish together.
+  // An explicit n_cb keeps the paper's static chunk order.
+  // Only worth it when a batch is long enough to hide the counter's atomic
+  // latency (>= 10 KB per stage; measured, profiles/r1_sweep.md).
+  const int dyn_env = env_int("TXB_DYNAMIC", -1);
+  g.dynamic = n_cb <= 0 && (dyn_env < 0 ? stage >= 10 * 1024 : dyn_env != 0);
+  if (g.dynamic) {
+    const int64_t n_batches = (n_cells + g.n_bc - 1) / g.n_bc;
+    g.grid = (int)std::max<int64_t>(1, std::min<int64_t>(n_batches, resident));
+  }
+  return TXB_OK;
+}
+
+// Device address of the dynamic-scheduling counter pool on the current device.
+static unsigned long long* work_pool_base() {
+  static std::mutex mu;
+  static std::vector<unsigned long long*> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if ((int)cache.size() <= dev) cache.resize(dev + 1, nullptr);
+  if (!cache[dev]) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, g_work_pool) != cudaSuccess) {
+      cuda_fail(cudaGetLastError(), "cudaGetSymbolAddress(g_work_pool)");
+      return nullptr;
+    }
+    cache[dev] = (unsigned long long*)p;
+  }
+  return cache[dev];
+}
+
+template <typename T>
+static void fill_tab(Tabulation<T>& t, int n_q, int n_b, int d, const void* basis, const void* basis_der,
+                     const void* weights) {
+  memset(&t, 0, sizeof(t));
+  memcpy(t.B, basis, sizeof(T) * n_q * n_b);
+  memcpy(t.D, basis_der, sizeof(T) * n_q * n_b * d);
+  memcpy(t.W, weights, sizeof(T) * n_q);
+}
+
+
+}  // namespace txb

@@ -79,47 +79,21 @@ __global__ void iota_keys_kernel(int64_t n, const int64_t* __restrict__ cells, i
 // order (numpy evaluates a*b - c*d as two rounded products and a rounded
 // difference; the 3x3 determinant sums left to right).
 template <int D>
-__global__ void geometry_kernel(int64_t n, const double* __restrict__ X, const int64_t* __restrict__ cells,
+__global__ void geometry_kernel(int64_t n, const double* __restrict__ X_, const int64_t* __restrict__ cells,
                                 double* __restrict__ inv_j, double* __restrict__ det_j,
                                 unsigned long long* bad) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += stride) {
     const int64_t* cv = cells + c * (D + 1);
-    double v0[D], m[D][D];
-    const int64_t i0 = cv[0];
+    double X[D + 1][D];
 #pragma unroll
-    for (int i = 0; i < D; ++i) v0[i] = X[i0 * D + i];
+    for (int b = 0; b <= D; ++b)
 #pragma unroll
-    for (int k = 0; k < D; ++k) {
-      const int64_t ik = cv[k + 1];
+      for (int i = 0; i < D; ++i) X[b][i] = X_[cv[b] * D + i];
+    double inv[D * D], det;
+    affine_inverse<D>(X, inv, det);
 #pragma unroll
-      for (int i = 0; i < D; ++i) m[i][k] = __dsub_rn(X[ik * D + i], v0[i]);  // column k = v_{k+1} - v_0
-    }
-    double* inv = inv_j + c * D * D;
-    double det;
-    if constexpr (D == 2) {
-      const double a = m[0][0], b = m[0][1], cc = m[1][0], e = m[1][1];
-      det = __dsub_rn(__dmul_rn(a, e), __dmul_rn(b, cc));
-      inv[0] = __ddiv_rn(e, det);
-      inv[1] = __ddiv_rn(-b, det);
-      inv[2] = __ddiv_rn(-cc, det);
-      inv[3] = __ddiv_rn(a, det);
-    } else {
-      const double cof00 = __dsub_rn(__dmul_rn(m[1][1], m[2][2]), __dmul_rn(m[1][2], m[2][1]));
-      const double cof01 = __dsub_rn(__dmul_rn(m[1][2], m[2][0]), __dmul_rn(m[1][0], m[2][2]));
-      const double cof02 = __dsub_rn(__dmul_rn(m[1][0], m[2][1]), __dmul_rn(m[1][1], m[2][0]));
-      det = __dadd_rn(__dadd_rn(__dmul_rn(m[0][0], cof00), __dmul_rn(m[0][1], cof01)),
-                      __dmul_rn(m[0][2], cof02));
-      inv[0 * 3 + 0] = __ddiv_rn(cof00, det);
-      inv[1 * 3 + 0] = __ddiv_rn(cof01, det);
-      inv[2 * 3 + 0] = __ddiv_rn(cof02, det);
-      inv[0 * 3 + 1] = __ddiv_rn(__dsub_rn(__dmul_rn(m[0][2], m[2][1]), __dmul_rn(m[0][1], m[2][2])), det);
-      inv[1 * 3 + 1] = __ddiv_rn(__dsub_rn(__dmul_rn(m[0][0], m[2][2]), __dmul_rn(m[0][2], m[2][0])), det);
-      inv[2 * 3 + 1] = __ddiv_rn(__dsub_rn(__dmul_rn(m[0][1], m[2][0]), __dmul_rn(m[0][0], m[2][1])), det);
-      inv[0 * 3 + 2] = __ddiv_rn(__dsub_rn(__dmul_rn(m[0][1], m[1][2]), __dmul_rn(m[0][2], m[1][1])), det);
-      inv[1 * 3 + 2] = __ddiv_rn(__dsub_rn(__dmul_rn(m[0][2], m[1][0]), __dmul_rn(m[0][0], m[1][2])), det);
-      inv[2 * 3 + 2] = __ddiv_rn(__dsub_rn(__dmul_rn(m[0][0], m[1][1]), __dmul_rn(m[0][1], m[1][0])), det);
-    }
+    for (int i = 0; i < D * D; ++i) inv_j[c * D * D + i] = inv[i];
     det_j[c] = det;
     if (det <= 0.0) atomicMin(bad, (unsigned long long)c);
   }

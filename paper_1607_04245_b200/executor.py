@@ -36,7 +36,7 @@ from .schedule import DEFAULT_THREAD_LIMIT, ExecutionGeometry, derive_execution_
 from .trace import ChunkTrace, ExecutionTrace, model_batch_counters, shared_image_bytes
 
 __all__ = ["DEFAULT_SHARED_MEM_LIMIT", "scalar_dtype", "execute_chunk", "integrate_transposed",
-           "integrate_cells"]
+           "integrate_cells", "integrate_mesh"]
 
 DEFAULT_SHARED_MEM_LIMIT = 48 * 1024
 _DTYPE_NAMES = {"f32": np.float32, "f64": np.float64}
@@ -183,17 +183,21 @@ def integrate_transposed(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule:
     torch = _torch()
     host_out = isinstance(coeffs_global, np.ndarray) or not hasattr(coeffs_global, "is_cuda")
     cells_dev = torch.from_numpy(np.ascontiguousarray(mesh.cells, dtype=np.int64)).to("cuda")
-
-    if cell_geom is None:
-        cell_geom = compute_geometry(mesh, cells=cells_dev, device_out=True)
     glob = coeffs_global if not host_out else np.asarray(coeffs_global, dtype=np.float64)
     glob_dev = _dev(glob, torch, dt)
-    blocks = gather_coefficients(mesh, layout, glob_dev, cells=cells_dev)
+    aux_dev = None if aux is None else CellAux(aux.space, _dev(aux.values, torch, dt))
 
-    elem = integrate_cells(
-        tab, rule, CellGeometry(_dev(cell_geom.inv_jacobians, torch, dt), _dev(cell_geom.determinants, torch, dt)),
-        blocks, None if aux is None else CellAux(aux.space, _dev(aux.values, torch, dt)), form,
-        dtype=dt, n_bl=n_bl, n_cb=n_cb)
+    if _mesh_fusable(tab, rule):
+        # geometry + gather + cast + integrate in one kernel (csrc/txb_integrate_mesh.cu)
+        elem = integrate_mesh(mesh, layout, tab, rule, form, glob_dev, aux_dev, dtype=dt, cell_geom=cell_geom,
+                              cells=cells_dev, n_bl=n_bl)
+    else:
+        if cell_geom is None:
+            cell_geom = compute_geometry(mesh, cells=cells_dev, device_out=True)
+        blocks = gather_coefficients(mesh, layout, glob_dev, cells=cells_dev)
+        elem = integrate_cells(
+            tab, rule, CellGeometry(_dev(cell_geom.inv_jacobians, torch, dt), _dev(cell_geom.determinants, torch, dt)),
+            blocks, aux_dev, form, dtype=dt, n_bl=n_bl, n_cb=n_cb)
     residual = scatter_add_element_vectors(mesh, layout, elem, incidence=_incidence_for(mesh, cells_dev))
 
     trace = ExecutionTrace(geom=geom, scalar_width=dt.itemsize, remainder_cells=geom.n_r)
@@ -203,3 +207,62 @@ def integrate_transposed(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule:
     if host_out:
         residual = residual.cpu().numpy()
     return residual, trace
+
+
+
+
+def _mesh_fusable(tab: Tabulation, rule: QuadratureRule) -> bool:
+    """The fused mesh kernel needs the standard P1 reference gradients (what
+    element.tabulate produces for every rule) and n_q <= 2."""
+    if rule.n_q > 2:
+        return False
+    D = np.asarray(tab.basis_der, dtype=np.float64)
+    want = np.vstack([-np.ones((1, tab.dim)), np.eye(tab.dim)])
+    return all(np.array_equal(D[q], want) for q in range(D.shape[0]))
+
+
+def integrate_mesh(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: QuadratureRule, form: PhysicsForm,
+                   coeffs_global, aux: Optional[CellAux] = None, *, dtype="f64", cell_geom=None, cells=None,
+                   out=None, n_bl: int = 0, check_orientation: bool = True):
+    """Element vectors straight from the mesh on the device: the reference's
+    compute_geometry -> gather_coefficients -> cast -> integrate_cells
+    (executor.py:194-212) fused into one kernel (txb_integrate_mesh).
+
+    ``coeffs_global``: (n_vertices * n_comp) CUDA tensor in the run dtype.
+    ``cell_geom``: None (geometry from the vertices, float64) or given geometry.
+    Returns a CUDA tensor (n_cells, n_b, n_comp).  Raises OrientationError
+    naming the first cell with detJ <= 0 (a host sync) when the geometry is
+    computed and ``check_orientation``."""
+    import ctypes
+
+    from . import _lib
+    from .errors import OrientationError
+
+    torch = _torch()
+    dt = scalar_dtype(dtype)
+    form.require_aux(aux)
+    kernel = _resolve_backend(None, form, rule.n_q, aux, dt.itemsize)
+    n = mesh.n_cells
+    C = cells if cells is not None else torch.from_numpy(np.ascontiguousarray(mesh.cells, dtype=np.int64)).cuda()
+    X = torch.from_numpy(np.ascontiguousarray(mesh.vertices, dtype=np.float64)).cuda()
+    g = _dev(coeffs_global, torch, dt)
+    if int(g.numel()) != mesh.n_vertices * form.n_comp:
+        raise ShapeError(f"global vector has {g.numel()} entries, expected {mesh.n_vertices * form.n_comp}")
+    inv = det = None
+    if cell_geom is not None:
+        inv, det = _dev(cell_geom.inv_jacobians, torch, dt), _dev(cell_geom.determinants, torch, dt)
+    av = None if aux is None else _dev(aux.values, torch, dt)
+    res = out if out is not None else torch.empty((n, tab.n_b, form.n_comp), dtype=g.dtype, device="cuda")
+    bad = torch.full((1,), -1, dtype=torch.int64, device="cuda") if cell_geom is None and check_orientation else None
+    B, D, W = (np.ascontiguousarray(x, dtype=dt) for x in (tab.basis, tab.basis_der, rule.weights))
+    ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
+    rc = _lib.lib().txb_integrate_mesh(
+        kernel[0], kernel[1], dt.itemsize, mesh.dim, rule.n_q, form.n_comp, n, mesh.n_vertices,
+        B.ctypes.data, D.ctypes.data, W.ctypes.data, X.data_ptr(), C.data_ptr(), g.data_ptr(), ptr(inv), ptr(det),
+        ptr(av), res.data_ptr(), ptr(bad), n_bl, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    _lib.check(rc, "txb_integrate_mesh")
+    if bad is not None:
+        i = int(bad.item())
+        if i >= 0:
+            raise OrientationError(f"cell {i} is degenerate or negatively oriented")
+    return res

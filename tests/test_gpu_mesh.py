@@ -48,3 +48,102 @@ def test_scatter_multiplicity_oracle():
     ones = txb.gather_coefficients(mesh, layout, np.ones(mesh.n_vertices))
     counts = txb.scatter_add_element_vectors(mesh, layout, ones)
     np.testing.assert_array_equal(counts, np.bincount(mesh.cells.ravel(), minlength=mesh.n_vertices))
+
+
+# ---- fused mesh kernel (txb_integrate_mesh): geometry + gather + cast + integrate ----
+
+import hashlib  # noqa: E402
+
+from conftest import BIG  # noqa: E402
+
+FORMS = [(txb.poisson_form, None), (txb.poisson_varcoef_form, "p0"), (txb.poisson_varcoef_form, "p1"),
+         (txb.elasticity_form, None)]
+
+
+def _mesh_problem(dim, n, factory, aux_space, seed, perturb=True):
+    mesh = txb.generate_unit_simplex_mesh(dim, n)
+    if perturb:  # non-grid vertices, still positively oriented
+        rng = np.random.default_rng(seed)
+        mesh = txb.Mesh(dim, mesh.vertices + 0.15 / n * rng.uniform(-1, 1, mesh.vertices.shape), mesh.cells)
+    form = factory(dim)
+    glob = np.random.default_rng(seed + 1).standard_normal(mesh.n_vertices * form.n_comp)
+    aux = None
+    if aux_space == "p0":
+        aux = txb.CellAux("p0", np.random.default_rng(seed + 2).uniform(0.5, 1.5, (mesh.n_cells, 1)))
+    elif aux_space == "p1":
+        nodal = np.random.default_rng(seed + 3).uniform(0.5, 1.5, (mesh.n_vertices, 1))
+        aux = txb.CellAux("p1", nodal[mesh.cells])
+    return mesh, form, glob, aux
+
+
+def _oracle_elem(mesh, form, glob, aux, rule, npdt):
+    inv, det = oracle.geometry(mesh.vertices, mesh.cells)
+    blocks = oracle.gather(mesh.cells, glob, form.n_comp)
+    tab = txb.tabulate(mesh.dim, rule)
+    fc = {"poisson": 0, "poisson_varcoef": 1, "elasticity": 2}[form.name]
+    am = {None: 0, "p0": 1, "p1": 2}[None if aux is None else aux.space]
+    return oracle.integrate(fc, am, tab.basis, tab.basis_der, rule.weights, inv, det, blocks,
+                            None if aux is None else aux.values, npdt), (inv, det)
+
+
+@pytest.mark.parametrize("dim,n", [(2, 23), (3, 7)])
+@pytest.mark.parametrize("factory,aux_space", FORMS)
+def test_fused_mesh_kernel_bitwise(dim, n, factory, aux_space):
+    mesh, form, glob, aux = _mesh_problem(dim, n, factory, aux_space, seed=5 * dim + n)
+    layout = txb.FieldLayout(form.n_comp)
+    for rule in (txb.quadrature_rule(dim, 1), txb.two_point_rule(dim)):
+        tab = txb.tabulate(dim, rule)
+        for dtype, npdt, tdt in (("f64", np.float64, torch.float64), ("f32", np.float32, torch.float32)):
+            ref, (inv, det) = _oracle_elem(mesh, form, glob, aux, rule, npdt)
+            g = torch.from_numpy(glob.astype(npdt)).cuda()
+            out = txb.integrate_mesh(mesh, layout, tab, rule, form, g, aux, dtype=dtype)
+            assert bitwise_equal(out.cpu().numpy(), ref), (dtype, rule.n_q, "geometry from vertices")
+            out = txb.integrate_mesh(mesh, layout, tab, rule, form, g, aux, dtype=dtype,
+                                     cell_geom=txb.CellGeometry(inv, det))
+            assert bitwise_equal(out.cpu().numpy(), ref), (dtype, rule.n_q, "given geometry")
+            for n_bl in (1, 5, 32):
+                out = txb.integrate_mesh(mesh, layout, tab, rule, form, g, aux, dtype=dtype, n_bl=n_bl)
+                assert bitwise_equal(out.cpu().numpy(), ref), (dtype, rule.n_q, n_bl)
+
+
+def test_fused_mesh_kernel_unaligned_connectivity():
+    mesh, form, glob, aux = _mesh_problem(3, 6, txb.poisson_varcoef_form, "p0", seed=9)
+    rule = txb.quadrature_rule(3, 1)
+    ref, _ = _oracle_elem(mesh, form, glob, aux, rule, np.float64)
+    buf = torch.empty(mesh.cells.size + 1, dtype=torch.int64, device="cuda")
+    cells = buf[1:].view(mesh.cells.shape)  # 8-byte aligned, not 16: direct global path
+    cells.copy_(torch.from_numpy(mesh.cells))
+    out = txb.integrate_mesh(mesh, txb.FieldLayout(1), txb.tabulate(3, rule), rule, form,
+                             torch.from_numpy(glob).cuda(), aux, dtype="f64", cells=cells)
+    assert bitwise_equal(out.cpu().numpy(), ref)
+
+
+def test_fused_mesh_kernel_orientation_error():
+    mesh = txb.Mesh(3, np.array([[0.0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [0, 0, -1]]),
+                    np.array([[0, 1, 2, 3], [0, 1, 2, 4]]))
+    rule = txb.quadrature_rule(3, 1)
+    with pytest.raises(txb.OrientationError, match="cell 1"):
+        txb.integrate_mesh(mesh, txb.FieldLayout(1), txb.tabulate(3, rule), rule, txb.poisson_form(3),
+                           torch.zeros(5, dtype=torch.float64, device="cuda"), None)
+
+
+@pytest.mark.parametrize("name", sorted(BIG))
+def test_fused_mesh_kernel_baseline_configs_by_hash(name):
+    """BASELINE configs[0..3] straight from the Kuhn mesh: bit-identical to the reference."""
+    e = BIG[name]
+    from paper_1607_04245_b200.workload import PHYSICS, refine_for
+
+    factory, aux_space = PHYSICS[e["physics"]]
+    form = factory(e["dim"])
+    full = txb.generate_unit_simplex_mesh(e["dim"], refine_for(e["dim"], e["n_cells"]))
+    mesh = txb.Mesh(e["dim"], full.vertices, np.ascontiguousarray(full.cells[:e["n_cells"]]))
+    glob = np.random.default_rng(e["seed"]).standard_normal(full.n_vertices * form.n_comp)
+    aux = None
+    if aux_space == "p0":
+        aux = txb.CellAux("p0", np.random.default_rng(e["seed"] + 1).uniform(0.5, 1.5, (full.n_cells, 1))[:e["n_cells"]])
+    rule = txb.quadrature_rule(e["dim"], 1)
+    for dtype, key, npdt in (("f64", "ref_f64", np.float64), ("f32", "cy_f32", np.float32)):
+        out = txb.integrate_mesh(mesh, txb.FieldLayout(form.n_comp), txb.tabulate(e["dim"], rule), rule, form,
+                                 torch.from_numpy(glob.astype(npdt)).cuda(), aux, dtype=dtype)
+        torch.cuda.synchronize()
+        assert hashlib.sha256(out.cpu().numpy().tobytes()).hexdigest() == e[key], (name, dtype)

@@ -237,6 +237,59 @@ def time_device(wl, steps, warmup, n_sets, barrier=None, sampler=None):
     return total, mode
 
 
+def time_mesh(name, steps, warmup, n_sets_min=4):
+    """Fused mesh kernel (geometry + gather + integrate, txb_integrate_mesh) on the
+    config's Kuhn mesh: connectivity/aux/out rotate over buffer sets (> L2);
+    vertex coordinates and the global coefficient vector are the mesh's own
+    (small, L2-resident by nature).  Returns (ms per launch, compulsory bytes per cell)."""
+    import torch
+
+    import paper_1607_04245_b200 as txb
+    from paper_1607_04245_b200.workload import PHYSICS, refine_for
+
+    dim, physics, dtype, n = CONFIGS[name]
+    factory, aux_space = PHYSICS[physics]
+    form = factory(dim)
+    full = txb.generate_unit_simplex_mesh(dim, refine_for(dim, n))
+    mesh = txb.Mesh(dim, full.vertices, np.ascontiguousarray(full.cells[:n]))
+    npdt = np.float32 if dtype == "f32" else np.float64
+    glob = torch.from_numpy(np.random.default_rng(1234).standard_normal(full.n_vertices * form.n_comp).astype(npdt)).cuda()
+    rule = txb.quadrature_rule(dim, 1)
+    tab = txb.tabulate(dim, rule)
+    s = np.dtype(npdt).itemsize
+    per_cell = (dim + 1) * 8 + (s if aux_space == "p0" else 0) + (dim + 1) * form.n_comp * s
+    n_sets = max(n_sets_min, -(-3 * L2_BYTES // (per_cell * n)) + 1)
+    cells0 = torch.from_numpy(mesh.cells).cuda()
+    verts = torch.from_numpy(np.ascontiguousarray(full.vertices)).cuda()
+    sets = []
+    for _ in range(n_sets):
+        aux = None
+        if aux_space == "p0":
+            aux = txb.CellAux("p0", torch.rand((n, 1), dtype=glob.dtype, device="cuda") + 0.5)
+        sets.append((cells0.clone(), aux, torch.empty((n, dim + 1, form.n_comp), dtype=glob.dtype, device="cuda")))
+
+    def launch(i):
+        cells, aux, out = sets[i % n_sets]
+        txb.integrate_mesh(mesh, txb.FieldLayout(form.n_comp), tab, rule, form, glob, aux, dtype=dtype,
+                           cells=cells, vertices=verts, out=out, check_orientation=False)
+
+    for i in range(warmup):
+        launch(i)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, capture_error_mode="relaxed"):
+        for i in range(steps):
+            launch(warmup + i)
+    graph.replay()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    graph.replay()
+    t1.record()
+    torch.cuda.synchronize()
+    return t0.elapsed_time(t1) / steps, per_cell
+
+
 class _null:
     def __enter__(self):
         return self
@@ -429,13 +482,28 @@ def main():
 
     import torch
 
-    torch.cuda.set_device(local)
+    # one process per GPU; TXB_BENCH_BACKEND=gloo (+ device = local % count) lets the
+    # multi-rank code path be exercised on a single-GPU box (timings then meaningless)
+    dist_backend = os.environ.get("TXB_BENCH_BACKEND", "nccl")
+    device = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(device)
     barrier = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+        else:
+            dist.init_process_group(dist_backend)
         barrier = dist.barrier
+
+    def reduce_max(x: float) -> float:
+        """max over ranks (timing of a multi-GPU step is the slowest rank)."""
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if dist_backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t[0])
 
     from paper_1607_04245_b200 import backend
 
@@ -444,12 +512,7 @@ def main():
     n_sets = max(4, -(-3 * L2_BYTES // set_bytes) + 1)
     sampler = ClockSampler(torch.cuda.current_device())
     total_ms, timing_mode = time_device(wl, args.steps, args.warmup, n_sets, barrier, sampler)
-    if world > 1:
-        import torch.distributed as dist
-
-        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t[0])
+    total_ms = reduce_max(total_ms)
     launch_ms = total_ms / args.steps  # one kernel launch per step
     cells_total = per_gpu * world
     ms_step = total_ms / args.steps
@@ -457,11 +520,10 @@ def main():
 
     # e2e through the host-buffer C ABI path
     e2e_steps = max(3, min(20, args.steps // 20))
+    if barrier:
+        barrier()
     e2e_s, h2d, d2h, _ = time_e2e(wl, e2e_steps, 2)
-    if world > 1:
-        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t[0])
+    e2e_s = reduce_max(e2e_s)
     e2e_gf = flops_cell * cells_total * e2e_steps / e2e_s / 1e9
 
     if rank != 0:
@@ -527,6 +589,24 @@ def main():
                              "bytes_per_cell": vb})
             del vw
             torch.cuda.empty_cache()
+        mesh_rows = []
+        for v in ("3d_varcoef_f64", "3d_varcoef_f32", "3d_elasticity_f64", "2d_varcoef_f64"):
+            vf, vb = config_model(v)
+            ms, per_cell = time_mesh(v, max(50, args.steps // 4), 5)
+            n = CONFIGS[v][3]
+            mesh_rows.append({"config": "mesh_" + v, "path": "txb_integrate_mesh (geometry+gather fused)",
+                              "cells": n, "launch_ms": ms, "gflops": vf * n / (ms * 1e-3) / 1e9,
+                              "gcells_per_s": n / (ms * 1e-3) / 1e9, "bytes_per_cell": per_cell,
+                              "gbs": per_cell * n / (ms * 1e-3) / 1e9,
+                              "frac": per_cell * n / (ms * 1e-3) / 1e9 / peak,
+                              "speedup_vs_cell_arrays_path": None})
+            for r in variants:
+                if r["config"] == v:
+                    mesh_rows[-1]["speedup_vs_cell_arrays_path"] = r["launch_ms"] / ms
+            if v == args.config:
+                mesh_rows[-1]["speedup_vs_cell_arrays_path"] = launch_ms / ms
+            torch.cuda.empty_cache()
+        variants.extend(mesh_rows)
         line["variants"] = variants
     print(json.dumps(line), flush=True)
 

@@ -223,13 +223,15 @@ def _mesh_fusable(tab: Tabulation, rule: QuadratureRule) -> bool:
 
 def integrate_mesh(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: QuadratureRule, form: PhysicsForm,
                    coeffs_global, aux: Optional[CellAux] = None, *, dtype="f64", cell_geom=None, cells=None,
-                   out=None, n_bl: int = 0, check_orientation: bool = True):
+                   vertices=None, out=None, n_bl: int = 0, check_orientation: bool = True):
     """Element vectors straight from the mesh on the device: the reference's
     compute_geometry -> gather_coefficients -> cast -> integrate_cells
     (executor.py:194-212) fused into one kernel (txb_integrate_mesh).
 
     ``coeffs_global``: (n_vertices * n_comp) CUDA tensor in the run dtype.
     ``cell_geom``: None (geometry from the vertices, float64) or given geometry.
+    ``cells`` / ``vertices``: optional device copies of the connectivity and
+    coordinates (uploaded from ``mesh`` otherwise).
     Returns a CUDA tensor (n_cells, n_b, n_comp).  Raises OrientationError
     naming the first cell with detJ <= 0 (a host sync) when the geometry is
     computed and ``check_orientation``."""
@@ -244,7 +246,8 @@ def integrate_mesh(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: Quadr
     kernel = _resolve_backend(None, form, rule.n_q, aux, dt.itemsize)
     n = mesh.n_cells
     C = cells if cells is not None else torch.from_numpy(np.ascontiguousarray(mesh.cells, dtype=np.int64)).cuda()
-    X = torch.from_numpy(np.ascontiguousarray(mesh.vertices, dtype=np.float64)).cuda()
+    X = vertices if vertices is not None else \
+        torch.from_numpy(np.ascontiguousarray(mesh.vertices, dtype=np.float64)).cuda()
     g = _dev(coeffs_global, torch, dt)
     if int(g.numel()) != mesh.n_vertices * form.n_comp:
         raise ShapeError(f"global vector has {g.numel()} entries, expected {mesh.n_vertices * form.n_comp}")

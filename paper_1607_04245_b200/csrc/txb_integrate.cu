@@ -64,6 +64,7 @@ struct IntegrateArgs {
   int bulk;    // 1: full batches arrive by bulk copy; 0: every batch read from global
   unsigned long long* work;  // dynamic mode: {next batch, CTAs done}, self-resetting; NULL = static chunks
   int64_t static_batches;    // dynamic mode: batches dealt round-robin before the counter takes over
+  int prefetch;              // batches per CTA warmed into L2 before the programmatic-launch wait
   Tabulation<T> tab;
 };
 
@@ -233,6 +234,19 @@ integrate_kernel(const __grid_constant__ IntegrateArgs<T> a) {
   unsigned char* scratch_base = smem + a.stages * stage_bytes;
   const PipelineSmem p = carve_pipeline(scratch_base + W * S::BYTES);
   pipeline_init(a, p);
+  if (warp == W && lane == 0 && a.bulk) {
+    // warm L2 with this CTA's first batches while the previous grid drains
+    pipeline_first_batches(a, a.prefetch, [&](int64_t c0, int ncell) {
+      const uint32_t ib = ncell * DD * sizeof(T), db = ncell * sizeof(T), cb = ncell * NBC * sizeof(T),
+                     ab = ncell * L::AUXW * sizeof(T);
+      if ((ib | db | cb | ab) & 15u) return;
+      bulk_prefetch_l2(a.inv_j + c0 * DD, ib);
+      bulk_prefetch_l2(a.det_j + c0, db);
+      bulk_prefetch_l2(a.coeffs + c0 * NBC, cb);
+      if constexpr (AUX != 0) bulk_prefetch_l2(a.aux + c0 * L::AUXW, ab);
+    });
+  }
+  pipeline_wait_prior_grid();
 
   if (warp == W) {
     // ============================ producer warp ============================
@@ -376,6 +390,7 @@ static int launch_t(const Config& c, const KernelInfo& k, const Geometry& g, int
   a.bulk = al16(inv_j) && al16(det_j) && al16(coeffs) && (c.aux == 0 || al16(aux)) && sized16(c.dim * c.dim) &&
            sized16(1) && sized16(nb * c.n_comp) && (c.aux == 0 || sized16(auxw)) &&
            env_int("TXB_DISABLE_BULK", 0) == 0;
+  a.prefetch = prefetch_batches(g);
   fill_tab(a.tab, c.n_q, c.dim + 1, c.dim, basis, basis_der, weights);
   void* params[] = {&a};
   cudaLaunchConfig_t cfg = {};

@@ -39,6 +39,7 @@ struct MeshArgs {
   int bulk;
   unsigned long long* work;
   int64_t static_batches;
+  int prefetch;  // batches per CTA warmed into L2 before the programmatic-launch wait
   Tabulation<T> tab;
 };
 
@@ -226,6 +227,20 @@ integrate_mesh_kernel(const __grid_constant__ MeshArgs<T> a) {
   unsigned char* scratch_base = smem + a.stages * stage_bytes;
   const PipelineSmem p = carve_pipeline(scratch_base + W * S::BYTES);
   pipeline_init(a, p);
+  if (warp == W && lane == 0 && a.bulk) {
+    pipeline_first_batches(a, a.prefetch, [&](int64_t c0, int ncell) {
+      const uint32_t kb = ncell * NB * 8, ab = ncell * L::AUXW * sizeof(T),
+                     ib = GEOM ? ncell * DD * sizeof(T) : 0, db = GEOM ? ncell * sizeof(T) : 0;
+      if ((kb | ab | ib | db) & 15u) return;
+      bulk_prefetch_l2(a.cells + c0 * NB, kb);
+      if constexpr (AUX != 0) bulk_prefetch_l2(a.aux + c0 * L::AUXW, ab);
+      if constexpr (GEOM != 0) {
+        bulk_prefetch_l2(a.inv_j + c0 * DD, ib);
+        bulk_prefetch_l2(a.det_j + c0, db);
+      }
+    });
+  }
+  pipeline_wait_prior_grid();
 
   if (warp == W) {
     if (lane != 0) return;
@@ -345,6 +360,7 @@ static int launch_mesh(const Config& c, const KernelInfo& k, const Geometry& g, 
     const int pct = std::min(100, std::max(0, env_int("TXB_STATIC_PCT", 60)));
     a.static_batches = n_batches * pct / 100 / g.grid * g.grid;
   }
+  a.prefetch = prefetch_batches(g);
   fill_tab(a.tab, c.n_q, c.dim + 1, c.dim, basis, basis_der, weights);
   void* params[] = {&a};
   cudaLaunchConfig_t cfg = {};

@@ -152,10 +152,32 @@ __device__ __forceinline__ void pipeline_init(const Args& a, const PipelineSmem&
     fence_mbar_init();
   }
   __syncthreads();
-  // Programmatic dependent launch: everything above overlapped the previous
-  // grid in the stream; from here on we touch global memory, so wait for it
-  // (no-op when launched without the PDL attribute), then let the next grid
-  // start its own prologue as our CTAs retire.
+}
+
+// First cells of this CTA's first `count` batches (for L2 prefetch before the
+// programmatic-launch wait): calls f(c0, ncell) for each.
+template <class Args, class F>
+__device__ __forceinline__ void pipeline_first_batches(const Args& a, int count, F f) {
+  const int nbc = a.n_bc;
+  if (a.work) {
+    for (int64_t b = blockIdx.x; count > 0 && b < a.static_batches; b += gridDim.x, --count) {
+      const int64_t c0 = b * nbc;
+      f(c0, (int)min((int64_t)nbc, a.n_cells - c0));
+    }
+  } else if ((int64_t)blockIdx.x < a.n_chunks) {
+    const int64_t lo = (int64_t)blockIdx.x * a.chunk_cells;
+    const int64_t hi = min(a.n_cells, lo + a.chunk_cells);
+    for (int64_t c0 = lo; count > 0 && c0 < hi; c0 += nbc, --count) f(c0, (int)min((int64_t)nbc, hi - c0));
+  }
+}
+
+// Programmatic dependent launch: everything before this overlapped the
+// previous grid in the stream (barrier setup and L2 prefetches, which return
+// no data and so cannot observe a value the previous grid is still writing);
+// from here on we read and write global memory, so wait for it (a no-op when
+// launched without the PDL attribute), then let the next grid start its own
+// prologue as our CTAs retire.
+__device__ __forceinline__ void pipeline_wait_prior_grid() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
@@ -502,6 +524,13 @@ static unsigned long long* work_pool_base() {
     cache[dev] = (unsigned long long*)p;
   }
   return cache[dev];
+}
+
+// Batches per CTA to warm into L2 before the programmatic-launch wait
+// (TXB_PREFETCH_BATCHES; default: the ring depth).
+static int prefetch_batches(const Geometry& g) {
+  const int v = env_int("TXB_PREFETCH_BATCHES", -1);
+  return v < 0 ? g.stages : v;
 }
 
 template <typename T>

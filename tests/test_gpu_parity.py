@@ -222,3 +222,25 @@ def test_max_size_fp32_3d_2_27_cells():
     txb.integrate_cells(w.tab, w.rule, txb.CellGeometry(inv_b, det_b), ones, aux_b, w.form, dtype="f32", out=out)
     torch.cuda.synchronize()
     assert int((out != 0).sum()) == 0
+
+
+def test_back_to_back_launches_see_each_others_writes():
+    """Programmatic dependent launch + L2 prefetch before griddepcontrol.wait must
+    keep stream semantics: a launch that reads the previous launch's output (and
+    a torch kernel's in-place update) sees the new values, every time."""
+    B, D, W = oracle.p1_tables(3)
+    _, inv, det, coeffs, aux = oracle.workload(3, "varcoef_p0", 200_000, seed=21)
+    ti = torch.from_numpy(np.ascontiguousarray(inv)).cuda()
+    td = torch.from_numpy(np.ascontiguousarray(det)).cuda()
+    ta = CellAux("p0", torch.from_numpy(np.ascontiguousarray(aux)).cuda())
+    x = torch.from_numpy(np.ascontiguousarray(coeffs)).cuda()
+    bufs = [torch.empty_like(x) for _ in range(4)]
+    ref = coeffs.copy()
+    cur = x
+    for it in range(4):  # out_{k+1} = E(out_k), chained on one stream with no sync
+        backend.run_cuda((1, 1), B, D, W, ti, td, cur, ta, bufs[it])
+        cur = bufs[it]
+        cur.mul_(-1.0)  # a torch kernel rewrites the next launch's input in place
+        ref = -oracle.integrate(1, 1, B, D, W, inv, det, ref, aux)
+    torch.cuda.synchronize()
+    assert bitwise_equal(cur.cpu().numpy(), ref)

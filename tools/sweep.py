@@ -25,12 +25,13 @@ def main():
         wl = bench.rank_workload(name, 0, 1)
         n_sets = max(4, -(-3 * bench.L2_BYTES // (bpc * wl["n"])) + 1)
         best = None
-        knobs = os.environ.get("SWEEP_GRID", "cells=128,256 inflight=48,72 dyn=0,1 pct=50,75,90")
+        knobs = os.environ.get("SWEEP_GRID", "cells=128,256 inflight=48,72 dyn=0,1 pct=50,75,90 pf=-1")
         kv = dict(x.split("=") for x in knobs.split())
-        grid = [(int(c), int(i), int(dy), int(pc)) for c in kv["cells"].split(",")
+        grid = [(int(c), int(i), int(dy), int(pc), int(pf)) for c in kv["cells"].split(",")
                 for i in kv["inflight"].split(",") for dy in kv["dyn"].split(",")
-                for pc in (kv["pct"].split(",") if dy == "1" else ["0"])]
-        for threads, smem, pdl, pct in grid:
+                for pc in (kv["pct"].split(",") if dy == "1" else ["0"]) for pf in kv.get("pf", "-1").split(",")]
+        for threads, smem, pdl, pct, pf in grid:
+            os.environ["TXB_PREFETCH_BATCHES"] = str(pf)
             os.environ["TXB_STATIC_PCT"] = str(pct)
             os.environ["TXB_TARGET_CELLS"] = str(threads)
             os.environ["TXB_INFLIGHT_KB"] = str(smem)
@@ -48,13 +49,13 @@ def main():
             w = 4 if wl["dtype"] == "f32" else 8
             cfg = backend.launch_config(*backend.cuda_kernel(form, 1, wl["aux"], w), w, wl["dim"], 1,
                                         form.n_comp, wl["n"])
-            rec = {"config": name, "cells": threads, "inflight_kb": smem, "dynamic": pdl, "static_pct": pct, "gbs": round(gbs, 1),
+            rec = {"config": name, "cells": threads, "inflight_kb": smem, "dynamic": pdl, "static_pct": pct, "prefetch": pf, "gbs": round(gbs, 1),
                    "frac": round(gbs / peak, 3), "us": round(ms * 1e3, 2), **cfg}
             print(json.dumps(rec), flush=True)
             if best is None or gbs > best["gbs"]:
                 best = rec
         print("BEST", json.dumps(best), flush=True)
-        for k in ("TXB_TARGET_CELLS", "TXB_INFLIGHT_KB", "TXB_DYNAMIC", "TXB_STATIC_PCT"):
+        for k in ("TXB_TARGET_CELLS", "TXB_INFLIGHT_KB", "TXB_DYNAMIC", "TXB_STATIC_PCT", "TXB_PREFETCH_BATCHES"):
             os.environ.pop(k, None)
         del wl
         torch.cuda.empty_cache()

@@ -142,7 +142,7 @@ int txb_gather_coefficients(int dtype_bytes, int64_t n_cells, int n_b, int n_com
  * txb_build_incidence, entries in ascending cell order, so every vertex sum
  * runs in the reference's np.add.at order (bit-identical). */
 int txb_scatter_add(int dtype_bytes, int64_t n_vertices, int n_comp,
-                    const int64_t* offsets, const int64_t* incidence,
+                    const int64_t* offsets, const int32_t* incidence,
                     const void* elem, void* out, void* stream);
 
 /* Build the vertex incidence CSR on the device from the connectivity
@@ -150,7 +150,7 @@ int txb_scatter_add(int dtype_bytes, int64_t n_vertices, int n_comp,
  * n_cells*n_b; `scratch` needs txb_incidence_scratch_bytes(...) bytes. */
 int64_t txb_incidence_scratch_bytes(int64_t n_cells, int n_b, int64_t n_vertices);
 int txb_build_incidence(int64_t n_cells, int n_b, int64_t n_vertices, const int64_t* cells,
-                        int64_t* offsets, int64_t* incidence, void* scratch, void* stream);
+                        int64_t* offsets, int32_t* incidence, void* scratch, void* stream);
 
 /* Per-cell inverse Jacobians and determinants from vertex coordinates
  * (device pointers, float64 like mesh.compute_geometry).  Returns

@@ -48,29 +48,48 @@ __global__ void gather_kernel(int64_t n_out, int n_b, int n_comp, const int64_t*
 
 // ---- scatter-add: one thread per (vertex, component), sums its incident
 // element entries in ascending (cell, b) order starting from +0, exactly the
-// sequence np.add.at applies (mesh.py:232-233).
-template <typename T>
-__global__ void scatter_kernel(int64_t n_vertices, int n_comp, const int64_t* __restrict__ offsets,
-                               const int64_t* __restrict__ incidence, const T* __restrict__ elem,
-                               T* __restrict__ out) {
-  const int64_t n = n_vertices * n_comp;
+// sequence np.add.at applies (mesh.py:232-233).  The incidence list is read
+// U entries at a time so U element loads are in flight per thread; the
+// NCOMP threads of a vertex read the same element rows (shared sectors).
+// (Measured alternatives -- one thread per vertex for all components, and a
+// shared-memory staged CSR range per CTA -- were slower; profiles/r1_pipeline.md.)
+constexpr int SCATTER_TPB = 256;
+
+template <typename T, int NCOMP>
+__global__ void __launch_bounds__(SCATTER_TPB)
+scatter_kernel(int64_t n_vertices, const int64_t* __restrict__ offsets, const int32_t* __restrict__ incidence,
+               const T* __restrict__ elem, T* __restrict__ out) {
+  constexpr int U = 8;
+  const int64_t n = n_vertices * NCOMP;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < n; o += stride) {
-    const int64_t v = o / n_comp;
-    const int k = (int)(o - v * n_comp);
-    T s = T(0);
-    for (int64_t e = offsets[v]; e < offsets[v + 1]; ++e) s = add(s, elem[incidence[e] * n_comp + k]);
-    out[o] = s;
+    const int64_t v = NCOMP == 1 ? o : o / NCOMP;
+    const int k = NCOMP == 1 ? 0 : (int)(o - v * NCOMP);
+    int64_t e = offsets[v];
+    const int64_t end = offsets[v + 1];
+    T sum = T(0);
+    for (; e < end; e += U) {
+      int32_t idx[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) idx[u] = e + u < end ? __ldg(incidence + e + u) : -1;
+      T val[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) val[u] = idx[u] >= 0 ? __ldg(elem + (int64_t)idx[u] * NCOMP + k) : T(0);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (idx[u] >= 0) sum = add(sum, val[u]);
+    }
+    out[o] = sum;
   }
 }
 
-__global__ void iota_keys_kernel(int64_t n, const int64_t* __restrict__ cells, int64_t* keys,
-                                 int64_t* vals, int64_t* counts) {
+__global__ void iota_keys_kernel(int64_t n, const int64_t* __restrict__ cells, int32_t* keys, int32_t* vals,
+                                 int64_t* counts) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const int64_t v = cells[i];
-    keys[i] = v;
-    vals[i] = i;
+    keys[i] = (int32_t)v;
+    vals[i] = (int32_t)i;
     atomicAdd(reinterpret_cast<unsigned long long*>(counts + v), 1ull);
   }
 }
@@ -134,9 +153,9 @@ extern "C" int txb_gather_coefficients(int dtype_bytes, int64_t n_cells, int n_b
 }
 
 extern "C" int txb_scatter_add(int dtype_bytes, int64_t n_vertices, int n_comp, const int64_t* offsets,
-                               const int64_t* incidence, const void* elem, void* out, void* stream) {
-  if (n_vertices < 0 || n_comp < 1) {
-    set_error("scatter: bad sizes");
+                               const int32_t* incidence, const void* elem, void* out, void* stream) {
+  if (n_vertices < 0 || n_comp < 1 || n_comp > TXB_MAX_COMP) {
+    set_error("scatter: bad sizes (n_vertices=%lld, n_comp=%d)", (long long)n_vertices, n_comp);
     return TXB_E_SHAPE;
   }
   if (n_vertices == 0) return TXB_OK;
@@ -144,28 +163,34 @@ extern "C" int txb_scatter_add(int dtype_bytes, int64_t n_vertices, int n_comp, 
     set_error("scatter: NULL device pointer");
     return TXB_E_ARG;
   }
-  const int64_t n = n_vertices * n_comp;
-  cudaStream_t s = (cudaStream_t)stream;
-  if (dtype_bytes == 8)
-    scatter_kernel<double><<<blocks_for(n), TPB, 0, s>>>(n_vertices, n_comp, offsets, incidence,
-                                                         (const double*)elem, (double*)out);
-  else if (dtype_bytes == 4)
-    scatter_kernel<float><<<blocks_for(n), TPB, 0, s>>>(n_vertices, n_comp, offsets, incidence,
-                                                        (const float*)elem, (float*)out);
-  else {
+  if (dtype_bytes != 4 && dtype_bytes != 8) {
     set_error("dtype_bytes must be 4 or 8");
     return TXB_E_UNSUPPORTED;
   }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int blocks = (int)std::min<int64_t>((n_vertices * n_comp + SCATTER_TPB - 1) / SCATTER_TPB, 1 << 20);
+#define TXB_SCATTER(T, NC)                                                                                  \
+  scatter_kernel<T, NC><<<blocks, SCATTER_TPB, 0, s>>>(n_vertices, offsets, incidence, (const T*)elem, (T*)out)
+  if (dtype_bytes == 8) {
+    if (n_comp == 1) TXB_SCATTER(double, 1);
+    else if (n_comp == 2) TXB_SCATTER(double, 2);
+    else TXB_SCATTER(double, 3);
+  } else {
+    if (n_comp == 1) TXB_SCATTER(float, 1);
+    else if (n_comp == 2) TXB_SCATTER(float, 2);
+    else TXB_SCATTER(float, 3);
+  }
+#undef TXB_SCATTER
   TXB_CUDA_TRY(cudaGetLastError());
   return TXB_OK;
 }
 
-// Scratch: keys_in, keys_out, vals_in (n*n_b each), counts (n_vertices+1),
-// CUB temp storage for the radix sort and the scan.
+// Scratch: keys_in, keys_out, vals_in (int32, n*n_b each), counts (int64,
+// n_vertices+1), CUB temp storage for the radix sort and the scan.
 static size_t cub_temp_bytes(int64_t n_entries, int64_t n_vertices) {
   size_t sort_b = 0, scan_b = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, sort_b, (const int64_t*)nullptr, (int64_t*)nullptr,
-                                  (const int64_t*)nullptr, (int64_t*)nullptr, (int64_t)n_entries);
+  cub::DeviceRadixSort::SortPairs(nullptr, sort_b, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                  (const int32_t*)nullptr, (int32_t*)nullptr, (int64_t)n_entries);
   cub::DeviceScan::ExclusiveSum(nullptr, scan_b, (const int64_t*)nullptr, (int64_t*)nullptr,
                                 (int64_t)(n_vertices + 1));
   return std::max(sort_b, scan_b);
@@ -175,14 +200,18 @@ static size_t a256(size_t x) { return (x + 255) / 256 * 256; }
 
 extern "C" int64_t txb_incidence_scratch_bytes(int64_t n_cells, int n_b, int64_t n_vertices) {
   const int64_t n = n_cells * n_b;
-  return (int64_t)(3 * a256(n * sizeof(int64_t)) + a256((n_vertices + 1) * sizeof(int64_t)) +
+  return (int64_t)(3 * a256(n * sizeof(int32_t)) + a256((n_vertices + 1) * sizeof(int64_t)) +
                    a256(cub_temp_bytes(n, n_vertices)));
 }
 
 extern "C" int txb_build_incidence(int64_t n_cells, int n_b, int64_t n_vertices, const int64_t* cells,
-                                   int64_t* offsets, int64_t* incidence, void* scratch, void* stream) {
+                                   int64_t* offsets, int32_t* incidence, void* scratch, void* stream) {
   if (n_cells < 0 || n_b < 1 || n_vertices < 0) {
     set_error("incidence: bad sizes");
+    return TXB_E_SHAPE;
+  }
+  if (n_cells * n_b >= ((int64_t)1 << 31) || n_vertices >= ((int64_t)1 << 31)) {
+    set_error("incidence: n_cells*n_b and n_vertices must be < 2^31 (int32 CSR)");
     return TXB_E_SHAPE;
   }
   if (!offsets || (n_cells > 0 && (!cells || !incidence || !scratch))) {
@@ -192,12 +221,12 @@ extern "C" int txb_build_incidence(int64_t n_cells, int n_b, int64_t n_vertices,
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t n = n_cells * n_b;
   unsigned char* p = (unsigned char*)scratch;
-  int64_t* keys_in = (int64_t*)p;
-  p += a256(n * sizeof(int64_t));
-  int64_t* keys_out = (int64_t*)p;
-  p += a256(n * sizeof(int64_t));
-  int64_t* vals_in = (int64_t*)p;
-  p += a256(n * sizeof(int64_t));
+  int32_t* keys_in = (int32_t*)p;
+  p += a256(n * sizeof(int32_t));
+  int32_t* keys_out = (int32_t*)p;
+  p += a256(n * sizeof(int32_t));
+  int32_t* vals_in = (int32_t*)p;
+  p += a256(n * sizeof(int32_t));
   int64_t* counts = (int64_t*)p;
   p += a256((n_vertices + 1) * sizeof(int64_t));
   void* temp = p;
@@ -210,7 +239,7 @@ extern "C" int txb_build_incidence(int64_t n_cells, int n_b, int64_t n_vertices,
     // Stable LSD radix sort by vertex id: entries of one vertex keep their
     // ascending (cell, b) order.
     int end_bit = 1;
-    while (end_bit < 63 && ((int64_t)1 << end_bit) < n_vertices) ++end_bit;
+    while (end_bit < 31 && ((int64_t)1 << end_bit) < n_vertices) ++end_bit;
     TXB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(temp, temp_b, keys_in, keys_out, vals_in, incidence,
                                                  (int64_t)n, 0, end_bit, s));
   }

@@ -205,7 +205,7 @@ def build_incidence(mesh: Mesh, cells=None) -> VertexIncidence:
     n, n_b, nv = int(C.shape[0]), mesh.dim + 1, mesh.n_vertices
     L = _lib.lib()
     offsets = torch.empty((nv + 1,), dtype=torch.int64, device="cuda")
-    inc = torch.empty((max(n * n_b, 1),), dtype=torch.int64, device="cuda")
+    inc = torch.empty((max(n * n_b, 1),), dtype=torch.int32, device="cuda")
     scratch = torch.empty((max(int(L.txb_incidence_scratch_bytes(n, n_b, nv)), 16),), dtype=torch.uint8,
                           device="cuda")
     _lib.check(L.txb_build_incidence(n, n_b, nv, C.data_ptr(), offsets.data_ptr(), inc.data_ptr(),

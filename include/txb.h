@@ -18,6 +18,12 @@
  *   txb_gather_coefficients   <- txfem/mesh.py:202-217 gather_coefficients
  *   txb_scatter_add           <- txfem/mesh.py:220-234 scatter_add_element_vectors
  *   txb_compute_geometry      <- txfem/mesh.py:150-190 compute_geometry
+ *   txb_jit_compile / txb_jit_integrate
+ *                          <- txfem/physics.py:260-304 user_form + the string-
+ *                             injection sources (physics.py:110-168) and
+ *                             txfem/codegen.py:50-256 generate_kernel_source,
+ *                             executed by the python lane
+ *                             txfem/_kernels_py.py:20-110 (f0, n_aux, grad a)
  *   txb_last_error         error text for the Python exception message
  *
  * Codes follow the reference (backend.py:26-27):
@@ -63,6 +69,7 @@ extern "C" {
 #define TXB_E_ARG          -5  /* NULL pointer where data is required         -> ValueError */
 #define TXB_E_CUDA         -6  /* CUDA runtime error (text in txb_last_error) -> RuntimeError */
 #define TXB_E_ORIENTATION  -7  /* detJ <= 0 in txb_compute_geometry           -> OrientationError */
+#define TXB_E_COMPILE      -8  /* user physics source does not compile (NVRTC) -> CodegenError */
 
 #define TXB_MAX_DIM    3
 #define TXB_MAX_BASIS  4
@@ -158,6 +165,39 @@ int txb_build_incidence(int64_t n_cells, int n_b, int64_t n_vertices, const int6
  * detJ <= 0; synchronises on `stream` to read the flag. */
 int txb_compute_geometry(int dim, int64_t n_cells, const double* vertices, const int64_t* cells,
                          double* inv_j, double* det_j, int64_t* bad_cell, void* stream);
+
+/* ---- Run-time compiled user physics (NVRTC, sm_100a) -------------------
+ * The form's pointwise functions are source text in the reference's
+ * string-injection dialect (physics.py:110-112): real / realv (d-vector with
+ * .x .y [.z]) and
+ *   realv f1_<name>(const real u[], const realv gradU[], const real a[],
+ *                   const realv gradA[], int comp)
+ *   real  f0_<name>(...same arguments...)          (optional: source_f0 NULL)
+ * txb_jit_compile assembles the integration kernel around them (the batch
+ * pipeline of txb_integrate_cells; every chain in the numpy lane's order,
+ * _kernels_py.py:20-110, compiled with -fmad=false), compiles it with NVRTC
+ * and returns a process-lifetime handle (memoised on the generated text; no
+ * device needed).  aux_mode 0/1/2 = none/P0/P1 with n_aux fields (1..4; 0
+ * iff aux_mode 0); P0 aux (n, n_aux), P1 aux (n, n_b, n_aux); uses_grad_a
+ * computes gradA for P1 (zero otherwise, _kernels_py.py:93-110).
+ * TXB_E_COMPILE carries the NVRTC log in txb_last_error. */
+int txb_jit_compile(const char* name, const char* source_f1, const char* source_f0, int dtype_bytes,
+                    int dim, int n_q, int n_comp, int n_aux, int aux_mode, int uses_grad_a,
+                    void** kernel);
+
+/* The generated translation unit and the compiler log of a handle. */
+const char* txb_jit_source(void* kernel);
+const char* txb_jit_log(void* kernel);
+int64_t txb_jit_cubin_bytes(void* kernel);
+/* Copies the sm_100a cubin into dst when capacity suffices; returns its size. */
+int64_t txb_jit_cubin(void* kernel, void* dst, int64_t capacity);
+
+/* txb_integrate_cells for a run-time compiled form: same layouts, device
+ * pointers, host tables, asynchronous on `stream`; the first call on a
+ * device loads the module there. */
+int txb_jit_integrate(void* kernel, int64_t n_cells, const void* basis, const void* basis_der,
+                      const void* weights, const void* inv_j, const void* det_j, const void* coeffs,
+                      const void* aux, void* out, int n_bl, int n_cb, void* stream);
 
 /* STREAM-like probe at a given read:write byte ratio (device pointers):
  * reads `read_bytes` from src, writes `write_bytes` to dst, 16-byte vector

@@ -13,13 +13,14 @@ import re
 from ctypes import c_char_p, c_int, c_int64, c_void_p, POINTER
 from pathlib import Path
 
-from .errors import (CapacityError, ConfigurationError, CudaLaneError, OrientationError,
+from .errors import (CapacityError, CodegenError, ConfigurationError, CudaLaneError, OrientationError,
                      ShapeError)
 
 LIB_PATH = Path(__file__).resolve().parent / "libtxb.so"
 
 TXB_OK, TXB_E_UNSUPPORTED, TXB_E_SHAPE, TXB_E_CONFIG = 0, -1, -2, -3
 TXB_E_CAPACITY, TXB_E_ARG, TXB_E_CUDA, TXB_E_ORIENTATION = -4, -5, -6, -7
+TXB_E_COMPILE = -8
 
 _I = c_int
 _P = c_void_p
@@ -38,6 +39,12 @@ SIGNATURES = {
     "txb_build_incidence": (_I, [c_int64, _I, c_int64, _P, _P, _P, _P, _P]),
     "txb_compute_geometry": (_I, [_I, c_int64, _P, _P, _P, _P, POINTER(c_int64), _P]),
     "txb_stream_probe": (_I, [_P, c_int64, _P, c_int64, _P]),
+    "txb_jit_compile": (_I, [c_char_p, c_char_p, c_char_p, _I, _I, _I, _I, _I, _I, _I, POINTER(c_void_p)]),
+    "txb_jit_source": (c_char_p, [_P]),
+    "txb_jit_log": (c_char_p, [_P]),
+    "txb_jit_cubin_bytes": (c_int64, [_P]),
+    "txb_jit_cubin": (c_int64, [_P, _P, c_int64]),
+    "txb_jit_integrate": (_I, [_P, c_int64] + [_P] * 8 + [_I, _I, _P]),
 }
 
 _lib = None
@@ -86,4 +93,6 @@ def check(rc: int, what: str = "txb") -> None:
         raise OrientationError(msg)
     if rc == TXB_E_ARG:
         raise ValueError(msg)
+    if rc == TXB_E_COMPILE:
+        raise CodegenError(msg)
     raise CudaLaneError(msg)

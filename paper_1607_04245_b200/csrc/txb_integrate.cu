@@ -48,25 +48,6 @@
 
 namespace txb {
 
-template <typename T>
-struct IntegrateArgs {
-  const T* inv_j;
-  const T* det_j;
-  const T* coeffs;
-  const T* aux;
-  T* out;
-  int64_t n_cells;
-  int64_t n_chunks;     // chunks, round-robin over the CTAs
-  int64_t chunk_cells;  // cells per chunk (a multiple of 16 or of N_bc)
-  int n_bc;    // cells per batch
-  int stages;  // ring depth
-  int warps;   // consumer warps
-  int bulk;    // 1: full batches arrive by bulk copy; 0: every batch read from global
-  unsigned long long* work;  // dynamic mode: {next batch, CTAs done}, self-resetting; NULL = static chunks
-  int64_t static_batches;    // dynamic mode: batches dealt round-robin before the counter takes over
-  int prefetch;              // batches per CTA warmed into L2 before the programmatic-launch wait
-  Tabulation<T> tab;
-};
 
 // One warp slice: CW cells starting at batch-local cell `c0` of a batch with
 // `ncell` cells whose per-cell arrays start at the given pointers (shared

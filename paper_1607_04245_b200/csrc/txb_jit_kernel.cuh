@@ -1,0 +1,220 @@
+// txb_jit_kernel.cuh — the thread-transposed integration kernel for a
+// user-supplied physics form, compiled at run time by NVRTC (txb_jit.cu).
+//
+// Same schedule as the ahead-of-time kernel (txb_integrate.cu): persistent
+// warp-specialised CTAs, one producer lane bulk-copying batches into a ring
+// of shared-memory stages, consumer warps running the quadrature phase
+// (lane <-> (cell, q)), a warp-scope transposition and the basis phase
+// (lane <-> element entry (cell, b, c)).  What is generic here:
+//   * the pointwise f1 and optional f0 are the user's source strings
+//     (TXB_F1 / TXB_F0, the reference's f1_<name> / f0_<name> convention,
+//     txfem/codegen.py:215-221), inlined;
+//   * any number of auxiliary fields (TXB_NAUX), P0 or P1, with the P1
+//     gradient when the form asks for it (txfem/_kernels_py.py:93-110);
+//   * any tabulation (no standard-P1 shortcuts): every chain starts at +0 and
+//     runs in the numpy lane's order (txfem/_kernels_py.py:20-90), so the
+//     element vectors are bit-identical to the reference's python lane for
+//     sources that evaluate like their f1_many / f0_many.
+//
+// The including unit defines: real, TXB_DIM, TXB_NQ, TXB_NCOMP, TXB_NAUX,
+// TXB_AUX_MODE (0 none, 1 P0, 2 P1), TXB_HAS_F0, TXB_GRAD_A, TXB_F1 and, with
+// an f0, TXB_F0.
+#pragma once
+
+#include "txb_pipeline.cuh"
+
+namespace txb {
+namespace jit {
+
+constexpr int D = TXB_DIM, NB = D + 1, NQ = TXB_NQ, NCOMP = TXB_NCOMP;
+constexpr int NAUX = TXB_NAUX, AUXM = TXB_AUX_MODE, NAS = NAUX > 0 ? NAUX : 1;
+constexpr bool HAS_F0 = TXB_HAS_F0 != 0, GRAD_A = TXB_GRAD_A != 0;
+constexpr int DD = D * D, NBC = NB * NCOMP;
+constexpr int AUXW = AUXM == 1 ? NAUX : (AUXM == 2 ? NB * NAUX : 0);
+constexpr int CW = 32 / NQ;  // cells per warp slice
+constexpr int S = (int)sizeof(real);
+// warp-private exchange area: T[q][b][k], f1s[q][c][k], f0s[q][c] per cell (odd strides)
+constexpr int TRS = make_odd(NQ * NB * D);
+constexpr int F1S = make_odd(NQ * NCOMP * D);
+constexpr int F0S = HAS_F0 ? make_odd(NQ * NCOMP) : 0;
+constexpr int SCRATCH_BYTES = round_up(CW * (TRS + F1S + F0S) * S, 16);
+
+__device__ __forceinline__ int inv_bytes(int n) { return round_up(n * DD * S, 16); }
+__device__ __forceinline__ int det_bytes(int n) { return round_up(n * S, 16); }
+__device__ __forceinline__ int coef_bytes(int n) { return round_up(n * NBC * S, 16); }
+__device__ __forceinline__ int aux_bytes(int n) { return round_up(n * AUXW * S, 16); }
+
+__device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const real* __restrict__ s_inv,
+                                           const real* __restrict__ s_det, const real* __restrict__ s_coef,
+                                           const real* __restrict__ s_aux, real* __restrict__ scratch, int c0,
+                                           int ncell, real* __restrict__ out, int lane) {
+  real* s_tr = scratch;
+  real* s_f1 = s_tr + CW * TRS;
+  real* s_f0 = s_f1 + CW * F1S;
+  const int nc = min(CW, ncell - c0);
+
+  // ---------------- quadrature phase: lane <-> (cell, q) ----------------
+  const int lc = lane / NQ;
+  const int q = lane - lc * NQ;
+  if (lc < nc) {
+    const int cell = c0 + lc;
+    real J[DD];
+#pragma unroll
+    for (int m = 0; m < DD; ++m) J[m] = s_inv[cell * DD + m];
+    const real det = s_det[cell];
+
+    // pulled-back gradients T[b][k] = sum_j D[q][b][j] invJ[j][k]  (_kernels_py.py:78-90)
+    real tr[NB][D];
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        real acc = real(0);
+#pragma unroll
+        for (int j = 0; j < D; ++j) acc = add(acc, mul(tab.D[(q * NB + b) * D + j], J[j * D + k]));
+        tr[b][k] = acc;
+        s_tr[lc * TRS + (q * NB + b) * D + k] = acc;
+      }
+
+    // u and grad u at the point (_kernels_py.py:44-51)
+    real u[NCOMP];
+    realv gradU[NCOMP];
+#pragma unroll
+    for (int c = 0; c < NCOMP; ++c) {
+      u[c] = real(0);
+      gradU[c] = realv(real(0));
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+      for (int c = 0; c < NCOMP; ++c) {
+        const real cf = s_coef[cell * NBC + b * NCOMP + c];
+        u[c] = add(u[c], mul(cf, tab.B[q * NB + b]));
+#pragma unroll
+        for (int k = 0; k < D; ++k) gradU[c][k] = add(gradU[c][k], mul(cf, tr[b][k]));
+      }
+
+    // auxiliary fields (_kernels_py.py:93-110)
+    real a[NAS];
+    realv gradA[NAS];
+#pragma unroll
+    for (int j = 0; j < NAS; ++j) {
+      a[j] = real(0);
+      gradA[j] = realv(real(0));
+    }
+    if constexpr (AUXM == 1) {
+#pragma unroll
+      for (int j = 0; j < NAUX; ++j) a[j] = s_aux[cell * NAUX + j];
+    } else if constexpr (AUXM == 2) {
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int j = 0; j < NAUX; ++j) a[j] = add(a[j], mul(s_aux[(cell * NB + b) * NAUX + j], tab.B[q * NB + b]));
+      if constexpr (GRAD_A) {
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+          for (int j = 0; j < NAUX; ++j)
+#pragma unroll
+            for (int k = 0; k < D; ++k)
+              gradA[j][k] = add(gradA[j][k], mul(s_aux[(cell * NB + b) * NAUX + j], tr[b][k]));
+      }
+    }
+
+    // pointwise physics, scaled by detJ then w_q (_kernels_py.py:53-65)
+    const real w = tab.W[q];
+#pragma unroll
+    for (int c = 0; c < NCOMP; ++c) {
+      const realv f1 = TXB_F1(u, gradU, a, gradA, c);
+#pragma unroll
+      for (int k = 0; k < D; ++k) s_f1[lc * F1S + (q * NCOMP + c) * D + k] = mul(mul(f1[k], det), w);
+#if TXB_HAS_F0
+      const real f0 = TXB_F0(u, gradU, a, gradA, c);
+      s_f0[lc * F0S + q * NCOMP + c] = mul(mul(f0, det), w);
+#endif
+    }
+  }
+
+  __syncwarp();  // ==== transpose threads (warp scope) ====
+
+  // ------------- basis phase: lane <-> element entry (cell, b, c) -------------
+  real* o_base = out + (int64_t)c0 * NBC;
+  for (int o = lane; o < nc * NBC; o += 32) {
+    const int ec = o / NBC;
+    const int r = o - ec * NBC;
+    const int b = r / NCOMP;
+    const int c = r - b * NCOMP;
+    real e = real(0);  // _kernels_py.py:67-75: q-major, f0 term then the k terms
+#pragma unroll
+    for (int qq = 0; qq < NQ; ++qq) {
+      if constexpr (HAS_F0) e = add(e, mul(tab.B[qq * NB + b], s_f0[ec * F0S + qq * NCOMP + c]));
+#pragma unroll
+      for (int k = 0; k < D; ++k)
+        e = add(e, mul(s_tr[ec * TRS + (qq * NB + b) * D + k], s_f1[ec * F1S + (qq * NCOMP + c) * D + k]));
+    }
+    o_base[o] = e;
+  }
+  __syncwarp();  // scratch is reused by the next slice
+}
+
+}  // namespace jit
+}  // namespace txb
+
+// dynamic-scheduling counters of this module (zero at load, self-resetting)
+__device__ unsigned long long txb_jit_work_pool[4096][2];
+
+extern "C" __global__ void __launch_bounds__(txb::MAX_CTA_THREADS, 1)
+txb_jit_integrate(const __grid_constant__ txb::IntegrateArgs<real> a) {
+  using namespace txb;
+  using namespace txb::jit;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int nbc = a.n_bc;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int W = a.warps;
+  const int o_det = inv_bytes(nbc), o_coef = o_det + det_bytes(nbc), o_aux = o_coef + coef_bytes(nbc);
+  const int stage_bytes = o_aux + aux_bytes(nbc);
+  unsigned char* scratch_base = smem + a.stages * stage_bytes;
+  const PipelineSmem p = carve_pipeline(scratch_base + W * SCRATCH_BYTES);
+  pipeline_init(a, p);
+  if (warp == W && lane == 0 && a.bulk) {
+    pipeline_first_batches(a, a.prefetch, [&](int64_t c0, int ncell) {
+      const uint32_t ib = ncell * DD * S, db = ncell * S, cb = ncell * NBC * S, ab = ncell * AUXW * S;
+      if ((ib | db | cb | ab) & 15u) return;
+      bulk_prefetch_l2(a.inv_j + c0 * DD, ib);
+      bulk_prefetch_l2(a.det_j + c0, db);
+      bulk_prefetch_l2(a.coeffs + c0 * NBC, cb);
+      if (AUXW) bulk_prefetch_l2(a.aux + c0 * AUXW, ab);
+    });
+  }
+  pipeline_wait_prior_grid();
+
+  if (warp == W) {
+    // ============================ producer warp ============================
+    if (lane != 0) return;
+    const uint64_t policy = l2_evict_first_policy();
+    pipeline_produce(a, p, smem, stage_bytes, [&](unsigned char* st, int64_t c0, int ncell, uint64_t* bar) {
+      const uint32_t ib = ncell * DD * S, db = ncell * S, cb = ncell * NBC * S, ab = ncell * AUXW * S;
+      if (!a.bulk || ((ib | db | cb | ab) & 15u)) return false;
+      mbar_arrive_expect_tx(bar, ib + db + cb + ab);
+      bulk_g2s(st, a.inv_j + c0 * DD, ib, bar, policy);
+      bulk_g2s(st + o_det, a.det_j + c0, db, bar, policy);
+      bulk_g2s(st + o_coef, a.coeffs + c0 * NBC, cb, bar, policy);
+      if (AUXW) bulk_g2s(st + o_aux, a.aux + c0 * AUXW, ab, bar, policy);
+      return true;
+    });
+    return;
+  }
+
+  // ============================ consumer warps ============================
+  real* scratch = reinterpret_cast<real*>(scratch_base + warp * SCRATCH_BYTES);
+  pipeline_consume(a, p, smem, stage_bytes, [&](const unsigned char* st, int64_t c0, int ncell) {
+    real* out = a.out + c0 * NBC;
+    const real* g_aux = AUXW ? a.aux + c0 * AUXW : nullptr;
+    const real* s_inv = st ? reinterpret_cast<const real*>(st) : a.inv_j + c0 * DD;
+    const real* s_det = st ? reinterpret_cast<const real*>(st + o_det) : a.det_j + c0;
+    const real* s_coef = st ? reinterpret_cast<const real*>(st + o_coef) : a.coeffs + c0 * NBC;
+    const real* s_aux = st ? reinterpret_cast<const real*>(st + o_aux) : g_aux;
+    for (int c = warp * CW; c < ncell; c += W * CW)
+      warp_slice(a.tab, s_inv, s_det, s_coef, s_aux, scratch, c, ncell, out, lane);
+  });
+}

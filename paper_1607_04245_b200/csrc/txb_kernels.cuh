@@ -5,6 +5,7 @@
 #pragma once
 
 #include "txb_common.cuh"
+#include "txb_pipeline.cuh"
 
 #include <algorithm>
 #include <atomic>
@@ -17,20 +18,9 @@
 
 namespace txb {
 
-constexpr int MAX_D = TXB_MAX_DIM, MAX_B = TXB_MAX_BASIS, MAX_Q = TXB_MAX_QUAD;
-constexpr int MAX_CONSUMER_WARPS = 16;
-constexpr int MAX_STAGES = 8;
 constexpr int WORK_POOL = 4096;  // per-launch dynamic-scheduling counters (device globals, zero at load)
 // one pool per translation unit (static): each kernel family draws its own slots
 static __device__ unsigned long long g_work_pool[WORK_POOL][2];
-constexpr int MAX_CTA_THREADS = 32 * (MAX_CONSUMER_WARPS + 1);
-
-template <typename T>
-struct Tabulation {
-  T B[MAX_Q * MAX_B];          // basis[q][b]
-  T D[MAX_Q * MAX_B * MAX_D];  // basis_der[q][b][j]
-  T W[MAX_Q];                  // weights[q]
-};
 
 // Byte layout of one ring stage: four 16-byte aligned regions holding the
 // batch's contiguous slices of inv_j, det_j, coeffs and aux.
@@ -65,38 +55,6 @@ struct Scratch {
   static constexpr int BYTES = TR_BYTES + CW * F1S * (int)sizeof(T);
 };
 
-// Vectorised row load: N consecutive T at p (row starts are multiples of
-// N*sizeof(T) from a 16-byte aligned base); widest access the alignment allows.
-template <typename T, int N, bool VEC = true>
-__device__ __forceinline__ void load_row(const T* __restrict__ p, T (&r)[N]) {
-  constexpr int BYTES = N * (int)sizeof(T);
-  if constexpr (!VEC) {
-#pragma unroll
-    for (int i = 0; i < N; ++i) r[i] = p[i];
-  } else if constexpr (BYTES % 16 == 0) {
-    constexpr int V = 16 / sizeof(T);
-#pragma unroll
-    for (int i = 0; i < N; i += V) {
-      const uint4 v = *reinterpret_cast<const uint4*>(p + i);
-      memcpy(&r[i], &v, 16);
-    }
-  } else if constexpr (BYTES % 8 == 0) {
-    constexpr int V = 8 / sizeof(T);
-#pragma unroll
-    for (int i = 0; i < N; i += V) {
-      const uint2 v = *reinterpret_cast<const uint2*>(p + i);
-      memcpy(&r[i], &v, 8);
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < N; ++i) r[i] = p[i];
-  }
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
 // Exactness note (why the chains below may skip the reference's "acc = 0;
 // acc = acc + x" first step and its 0*x / 1*x products): in round-to-nearest
 // a sum is -0 only if both operands are -0, so a chain started at +0 is never
@@ -106,163 +64,6 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // either sign leaves the partial sum unchanged.  Hence only the final
 // element-vector chain must start at +0 to reproduce the reference bit for
 // bit; everything upstream may drop exact no-ops.  (Finite inputs.)
-
-// ---------------------------------------------------------------------------
-// The batch pipeline shared by every streaming kernel of the library.
-//
-// Args provides: n_cells, n_chunks, chunk_cells, n_bc, stages, warps, work,
-// static_batches.  One producer lane (warp `warps`, lane 0) walks the batch
-// sequence -- static contiguous chunks, or round-robin + a per-launch atomic
-// counter for the tail (`work` != NULL) -- and for each batch calls
-//     issue(stage_ptr, c0, ncell, full_bar)  -> true if it posted expect_tx and
-//                                              bulk copies, false if the batch
-//                                              must be read from global memory
-// Consumer warps wait on the stage's `full` barrier and call
-//     consume(stage_ptr or nullptr, c0, ncell)
-// then arrive on `empty`.  A count of 0 published in the stage info stops them.
-// ---------------------------------------------------------------------------
-struct PipelineSmem {
-  uint64_t* full;
-  uint64_t* empty;
-  int64_t* info_c0;
-  int* info_n;
-  int* warps_done;
-};
-
-// mbarriers + stage info + done counter, carved after `base`
-__device__ __forceinline__ PipelineSmem carve_pipeline(unsigned char* base) {
-  PipelineSmem p;
-  p.full = reinterpret_cast<uint64_t*>(base);
-  p.empty = p.full + MAX_STAGES;
-  p.info_c0 = reinterpret_cast<int64_t*>(p.empty + MAX_STAGES);
-  p.info_n = reinterpret_cast<int*>(p.info_c0 + MAX_STAGES);
-  p.warps_done = p.info_n + MAX_STAGES;
-  return p;
-}
-constexpr int PIPELINE_SMEM_BYTES = 8 * (3 * MAX_STAGES) + 4 * MAX_STAGES + 16;
-
-template <class Args>
-__device__ __forceinline__ void pipeline_init(const Args& a, const PipelineSmem& p) {
-  if (threadIdx.x == 0) {
-    *p.warps_done = 0;
-    for (int s = 0; s < a.stages; ++s) {
-      mbar_init(&p.full[s], 1);
-      mbar_init(&p.empty[s], a.warps);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-}
-
-// First cells of this CTA's first `count` batches (for L2 prefetch before the
-// programmatic-launch wait): calls f(c0, ncell) for each.
-template <class Args, class F>
-__device__ __forceinline__ void pipeline_first_batches(const Args& a, int count, F f) {
-  const int nbc = a.n_bc;
-  if (a.work) {
-    for (int64_t b = blockIdx.x; count > 0 && b < a.static_batches; b += gridDim.x, --count) {
-      const int64_t c0 = b * nbc;
-      f(c0, (int)min((int64_t)nbc, a.n_cells - c0));
-    }
-  } else if ((int64_t)blockIdx.x < a.n_chunks) {
-    const int64_t lo = (int64_t)blockIdx.x * a.chunk_cells;
-    const int64_t hi = min(a.n_cells, lo + a.chunk_cells);
-    for (int64_t c0 = lo; count > 0 && c0 < hi; c0 += nbc, --count) f(c0, (int)min((int64_t)nbc, hi - c0));
-  }
-}
-
-// Programmatic dependent launch: everything before this overlapped the
-// previous grid in the stream (barrier setup and L2 prefetches, which return
-// no data and so cannot observe a value the previous grid is still writing);
-// from here on we read and write global memory, so wait for it (a no-op when
-// launched without the PDL attribute), then let the next grid start its own
-// prologue as our CTAs retire.
-__device__ __forceinline__ void pipeline_wait_prior_grid() {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-
-template <class Args, class Issue>
-__device__ __forceinline__ void pipeline_produce(const Args& a, const PipelineSmem& p, unsigned char* stages,
-                                                 int stage_bytes, Issue issue) {
-  const int nbc = a.n_bc;
-  int stage = 0;
-  uint32_t phase = 0;
-  auto publish = [&](int64_t c0, int ncell) {
-    mbar_wait(&p.empty[stage], phase ^ 1);
-    p.info_c0[stage] = c0;
-    p.info_n[stage] = ncell;  // 0 = stop
-    if (ncell == 0 || !issue(stages + stage * stage_bytes, c0, ncell, &p.full[stage])) {
-      if (ncell) p.info_n[stage] = -ncell;  // consumers read this batch from global memory
-      mbar_arrive(&p.full[stage]);
-    }
-    if (++stage == a.stages) {
-      stage = 0;
-      phase ^= 1;
-    }
-  };
-  if (a.work) {
-    // dynamic: the first a.static_batches batches are dealt round-robin,
-    // the rest are grabbed from a per-launch counter so CTAs on SMs that
-    // get more bandwidth take more of the tail.  The next grab is issued
-    // before the current batch is published, hiding the atomic's latency.
-    const int64_t n_batches = (a.n_cells + nbc - 1) / nbc;
-    for (int64_t b = blockIdx.x; b < a.static_batches; b += gridDim.x) {
-      const int64_t c0 = b * nbc;
-      publish(c0, (int)min((int64_t)nbc, a.n_cells - c0));
-    }
-    int64_t next = a.static_batches + (int64_t)atomicAdd(a.work, 1ull);
-    while (next < n_batches) {
-      const int64_t b = next;
-      next = a.static_batches + (int64_t)atomicAdd(a.work, 1ull);
-      const int64_t c0 = b * nbc;
-      publish(c0, (int)min((int64_t)nbc, a.n_cells - c0));
-    }
-  } else {
-    // static: contiguous chunks, round-robin over the CTAs
-    for (int64_t ci = blockIdx.x; ci < a.n_chunks; ci += gridDim.x) {
-      const int64_t lo = ci * a.chunk_cells;
-      const int64_t hi = min(a.n_cells, lo + a.chunk_cells);
-      for (int64_t c0 = lo; c0 < hi; c0 += nbc) publish(c0, (int)min((int64_t)nbc, hi - c0));
-    }
-  }
-  publish(0, 0);  // stop
-}
-
-template <class Args, class Consume>
-__device__ __forceinline__ void pipeline_consume(const Args& a, const PipelineSmem& p, unsigned char* stages,
-                                                 int stage_bytes, Consume consume) {
-  const int lane = threadIdx.x & 31;
-  int stage = 0;
-  uint32_t phase = 0;
-  for (;;) {
-    mbar_wait(&p.full[stage], phase);
-    const int64_t c0 = p.info_c0[stage];
-    const int nsig = p.info_n[stage];
-    if (nsig == 0) break;
-    if (nsig > 0)
-      consume(stages + stage * stage_bytes, c0, nsig);
-    else
-      consume(nullptr, c0, -nsig);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&p.empty[stage]);
-    if (++stage == a.stages) {
-      stage = 0;
-      phase ^= 1;
-    }
-  }
-  // dynamic mode: the last CTA out resets the per-launch counters for the
-  // next launch that draws this slot (stream order / PDL wait make it visible)
-  if (a.work && lane == 0) {
-    if (atomicAdd(p.warps_done, 1) == a.warps - 1) {
-      __threadfence();
-      if (atomicAdd(a.work + 1, 1ull) == (unsigned long long)gridDim.x - 1) {
-        atomicExch(a.work, 0ull);
-        atomicExch(a.work + 1, 0ull);
-      }
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Host-side launch geometry (shared)
@@ -331,9 +132,21 @@ static void default_decomposition(const Config& c, int& n_bl, int& n_cb) {
 
 struct KernelInfo {
   void* fn;
-  int (*stage_bytes)(int);
-  int (*scratch)(int);  // per consumer warp
+  int (*stage_bytes)(int);  // NULL: run-time layout below (JIT kernels)
+  int (*scratch)(int);      // per consumer warp
   int cw;
+  // run-time stage layout: scalars per cell of each of the four ring regions,
+  // scalar width, scratch bytes per consumer warp (used when stage_bytes is NULL)
+  int rt_region[4];
+  int rt_s;
+  int rt_scratch;
+  int stage(int n_bc) const {
+    if (stage_bytes) return stage_bytes(n_bc);
+    int b = 0;
+    for (int r = 0; r < 4; ++r) b += round_up(n_bc * rt_region[r] * rt_s, 16);
+    return b;
+  }
+  int scratch_bytes(int n_bc) const { return scratch ? scratch(n_bc) : rt_scratch; }
 };
 
 // True when every tabulated reference gradient is exactly the P1 one:
@@ -399,8 +212,8 @@ static int compute_geometry(const Config& c, const KernelInfo& k, int64_t n_cell
   g.warps = std::min(wcap, slices);
   g.threads = 32 * (g.warps + 1);
 
-  const int stage = k.stage_bytes(g.n_bc);
-  const int fixed = g.warps * k.scratch(g.n_bc) + PIPELINE_SMEM_BYTES + 16;
+  const int stage = k.stage(g.n_bc);
+  const int fixed = g.warps * k.scratch_bytes(g.n_bc) + PIPELINE_SMEM_BYTES + 16;
   int smem_cap = 227 * 1024;
   int dev = 0, sms = 148;
   if (query_device && cudaGetDevice(&dev) == cudaSuccess) {

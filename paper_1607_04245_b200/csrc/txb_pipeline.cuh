@@ -1,0 +1,230 @@
+// txb_pipeline.cuh — the warp-specialised bulk-copy batch pipeline shared by
+// every streaming kernel of the library (cell-array integration, mesh-fused
+// integration, run-time compiled user physics).  Device code only: NVRTC
+// compiles this file from memory for the user-physics kernels (txb_jit.cu).
+#pragma once
+
+#include "txb_device.cuh"
+
+namespace txb {
+
+constexpr int MAX_D = TXB_MAX_DIM, MAX_B = TXB_MAX_BASIS, MAX_Q = TXB_MAX_QUAD;
+constexpr int MAX_CONSUMER_WARPS = 16;
+constexpr int MAX_STAGES = 8;
+constexpr int MAX_CTA_THREADS = 32 * (MAX_CONSUMER_WARPS + 1);
+
+template <typename T>
+struct Tabulation {
+  T B[MAX_Q * MAX_B];          // basis[q][b]
+  T D[MAX_Q * MAX_B * MAX_D];  // basis_der[q][b][j]
+  T W[MAX_Q];                  // weights[q]
+};
+
+// Kernel parameters of the cell-array integration kernels (ahead-of-time and
+// run-time compiled): one __grid_constant__ struct, tabulation included.
+template <typename T>
+struct IntegrateArgs {
+  const T* inv_j;
+  const T* det_j;
+  const T* coeffs;
+  const T* aux;
+  T* out;
+  int64_t n_cells;
+  int64_t n_chunks;     // chunks, round-robin over the CTAs
+  int64_t chunk_cells;  // cells per chunk (a multiple of 16 or of N_bc)
+  int n_bc;    // cells per batch
+  int stages;  // ring depth
+  int warps;   // consumer warps
+  int bulk;    // 1: full batches arrive by bulk copy; 0: every batch read from global
+  unsigned long long* work;  // dynamic mode: {next batch, CTAs done}, self-resetting; NULL = static chunks
+  int64_t static_batches;    // dynamic mode: batches dealt round-robin before the counter takes over
+  int prefetch;              // batches per CTA warmed into L2 before the programmatic-launch wait
+  Tabulation<T> tab;
+};
+
+// Vectorised row load: N consecutive T at p (row starts are multiples of
+// N*sizeof(T) from a 16-byte aligned base); widest access the alignment allows.
+template <typename T, int N, bool VEC = true>
+__device__ __forceinline__ void load_row(const T* __restrict__ p, T (&r)[N]) {
+  constexpr int BYTES = N * (int)sizeof(T);
+  if constexpr (!VEC) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) r[i] = p[i];
+  } else if constexpr (BYTES % 16 == 0) {
+    constexpr int V = 16 / sizeof(T);
+#pragma unroll
+    for (int i = 0; i < N; i += V) {
+      const uint4 v = *reinterpret_cast<const uint4*>(p + i);
+      __builtin_memcpy(&r[i], &v, 16);
+    }
+  } else if constexpr (BYTES % 8 == 0) {
+    constexpr int V = 8 / sizeof(T);
+#pragma unroll
+    for (int i = 0; i < N; i += V) {
+      const uint2 v = *reinterpret_cast<const uint2*>(p + i);
+      __builtin_memcpy(&r[i], &v, 8);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) r[i] = p[i];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// The batch pipeline shared by every streaming kernel of the library.
+//
+// Args provides: n_cells, n_chunks, chunk_cells, n_bc, stages, warps, work,
+// static_batches.  One producer lane (warp `warps`, lane 0) walks the batch
+// sequence -- static contiguous chunks, or round-robin + a per-launch atomic
+// counter for the tail (`work` != NULL) -- and for each batch calls
+//     issue(stage_ptr, c0, ncell, full_bar)  -> true if it posted expect_tx and
+//                                              bulk copies, false if the batch
+//                                              must be read from global memory
+// Consumer warps wait on the stage's `full` barrier and call
+//     consume(stage_ptr or nullptr, c0, ncell)
+// then arrive on `empty`.  A count of 0 published in the stage info stops them.
+// ---------------------------------------------------------------------------
+struct PipelineSmem {
+  uint64_t* full;
+  uint64_t* empty;
+  int64_t* info_c0;
+  int* info_n;
+  int* warps_done;
+};
+
+// mbarriers + stage info + done counter, carved after `base`
+__device__ __forceinline__ PipelineSmem carve_pipeline(unsigned char* base) {
+  PipelineSmem p;
+  p.full = reinterpret_cast<uint64_t*>(base);
+  p.empty = p.full + MAX_STAGES;
+  p.info_c0 = reinterpret_cast<int64_t*>(p.empty + MAX_STAGES);
+  p.info_n = reinterpret_cast<int*>(p.info_c0 + MAX_STAGES);
+  p.warps_done = p.info_n + MAX_STAGES;
+  return p;
+}
+constexpr int PIPELINE_SMEM_BYTES = 8 * (3 * MAX_STAGES) + 4 * MAX_STAGES + 16;
+
+template <class Args>
+__device__ __forceinline__ void pipeline_init(const Args& a, const PipelineSmem& p) {
+  if (threadIdx.x == 0) {
+    *p.warps_done = 0;
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(&p.full[s], 1);
+      mbar_init(&p.empty[s], a.warps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+}
+
+// First cells of this CTA's first `count` batches (for L2 prefetch before the
+// programmatic-launch wait): calls f(c0, ncell) for each.
+template <class Args, class F>
+__device__ __forceinline__ void pipeline_first_batches(const Args& a, int count, F f) {
+  const int nbc = a.n_bc;
+  if (a.work) {
+    for (int64_t b = blockIdx.x; count > 0 && b < a.static_batches; b += gridDim.x, --count) {
+      const int64_t c0 = b * nbc;
+      f(c0, (int)min((int64_t)nbc, a.n_cells - c0));
+    }
+  } else if ((int64_t)blockIdx.x < a.n_chunks) {
+    const int64_t lo = (int64_t)blockIdx.x * a.chunk_cells;
+    const int64_t hi = min(a.n_cells, lo + a.chunk_cells);
+    for (int64_t c0 = lo; count > 0 && c0 < hi; c0 += nbc, --count) f(c0, (int)min((int64_t)nbc, hi - c0));
+  }
+}
+
+// Programmatic dependent launch: everything before this overlapped the
+// previous grid in the stream (barrier setup and L2 prefetches, which return
+// no data and so cannot observe a value the previous grid is still writing);
+// from here on we read and write global memory, so wait for it (a no-op when
+// launched without the PDL attribute), then let the next grid start its own
+// prologue as our CTAs retire.
+__device__ __forceinline__ void pipeline_wait_prior_grid() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <class Args, class Issue>
+__device__ __forceinline__ void pipeline_produce(const Args& a, const PipelineSmem& p, unsigned char* stages,
+                                                 int stage_bytes, Issue issue) {
+  const int nbc = a.n_bc;
+  int stage = 0;
+  uint32_t phase = 0;
+  auto publish = [&](int64_t c0, int ncell) {
+    mbar_wait(&p.empty[stage], phase ^ 1);
+    p.info_c0[stage] = c0;
+    p.info_n[stage] = ncell;  // 0 = stop
+    if (ncell == 0 || !issue(stages + stage * stage_bytes, c0, ncell, &p.full[stage])) {
+      if (ncell) p.info_n[stage] = -ncell;  // consumers read this batch from global memory
+      mbar_arrive(&p.full[stage]);
+    }
+    if (++stage == a.stages) {
+      stage = 0;
+      phase ^= 1;
+    }
+  };
+  if (a.work) {
+    // dynamic: the first a.static_batches batches are dealt round-robin,
+    // the rest are grabbed from a per-launch counter so CTAs on SMs that
+    // get more bandwidth take more of the tail.  The next grab is issued
+    // before the current batch is published, hiding the atomic's latency.
+    const int64_t n_batches = (a.n_cells + nbc - 1) / nbc;
+    for (int64_t b = blockIdx.x; b < a.static_batches; b += gridDim.x) {
+      const int64_t c0 = b * nbc;
+      publish(c0, (int)min((int64_t)nbc, a.n_cells - c0));
+    }
+    int64_t next = a.static_batches + (int64_t)atomicAdd(a.work, 1ull);
+    while (next < n_batches) {
+      const int64_t b = next;
+      next = a.static_batches + (int64_t)atomicAdd(a.work, 1ull);
+      const int64_t c0 = b * nbc;
+      publish(c0, (int)min((int64_t)nbc, a.n_cells - c0));
+    }
+  } else {
+    // static: contiguous chunks, round-robin over the CTAs
+    for (int64_t ci = blockIdx.x; ci < a.n_chunks; ci += gridDim.x) {
+      const int64_t lo = ci * a.chunk_cells;
+      const int64_t hi = min(a.n_cells, lo + a.chunk_cells);
+      for (int64_t c0 = lo; c0 < hi; c0 += nbc) publish(c0, (int)min((int64_t)nbc, hi - c0));
+    }
+  }
+  publish(0, 0);  // stop
+}
+
+template <class Args, class Consume>
+__device__ __forceinline__ void pipeline_consume(const Args& a, const PipelineSmem& p, unsigned char* stages,
+                                                 int stage_bytes, Consume consume) {
+  const int lane = threadIdx.x & 31;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (;;) {
+    mbar_wait(&p.full[stage], phase);
+    const int64_t c0 = p.info_c0[stage];
+    const int nsig = p.info_n[stage];
+    if (nsig == 0) break;
+    if (nsig > 0)
+      consume(stages + stage * stage_bytes, c0, nsig);
+    else
+      consume(nullptr, c0, -nsig);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&p.empty[stage]);
+    if (++stage == a.stages) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+  // dynamic mode: the last CTA out resets the per-launch counters for the
+  // next launch that draws this slot (stream order / PDL wait make it visible)
+  if (a.work && lane == 0) {
+    if (atomicAdd(p.warps_done, 1) == a.warps - 1) {
+      __threadfence();
+      if (atomicAdd(a.work + 1, 1ull) == (unsigned long long)gridDim.x - 1) {
+        atomicExch(a.work, 0ull);
+        atomicExch(a.work + 1, 0ull);
+      }
+    }
+  }
+}
+
+}  // namespace txb

@@ -177,7 +177,7 @@ def integrate_transposed(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule:
     _check_capacity(geom, dt.itemsize, form.has_f0, shared_mem_limit)
     if log_tasks:
         raise ValueError("log_tasks is a simulated-device audit feature; not available on the cuda lane")
-    _resolve_backend(backend, form, rule.n_q, aux, dt.itemsize)
+    kernel = _resolve_backend(backend, form, rule.n_q, aux, dt.itemsize)
     if aux is not None and int(aux.values.shape[0]) != mesh.n_cells:
         raise ShapeError(f"auxiliary data covers {aux.values.shape[0]} cells, expected {mesh.n_cells}")
     torch = _torch()
@@ -187,7 +187,7 @@ def integrate_transposed(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule:
     glob_dev = _dev(glob, torch, dt)
     aux_dev = None if aux is None else CellAux(aux.space, _dev(aux.values, torch, dt))
 
-    if _mesh_fusable(tab, rule):
+    if _mesh_fusable(tab, rule) and not isinstance(kernel, _backend.JitKernel):
         # geometry + gather + cast + integrate in one kernel (csrc/txb_integrate_mesh.cu)
         elem = integrate_mesh(mesh, layout, tab, rule, form, glob_dev, aux_dev, dtype=dt, cell_geom=cell_geom,
                               cells=cells_dev, n_bl=n_bl)
@@ -244,6 +244,9 @@ def integrate_mesh(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: Quadr
     dt = scalar_dtype(dtype)
     form.require_aux(aux)
     kernel = _resolve_backend(None, form, rule.n_q, aux, dt.itemsize)
+    if isinstance(kernel, _backend.JitKernel):
+        raise ValueError(f"the fused mesh kernel covers the shipped forms; form {form.name!r} runs through "
+                         "integrate_transposed (geometry -> gather -> run-time compiled integration)")
     n = mesh.n_cells
     C = cells if cells is not None else torch.from_numpy(np.ascontiguousarray(mesh.cells, dtype=np.int64)).cuda()
     X = vertices if vertices is not None else \

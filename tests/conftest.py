@@ -64,3 +64,26 @@ def load_big_hashes():
 
 SMALL_CASES = load_small_cases()
 BIG = load_big_hashes()
+
+
+class UserCase:
+    """A user-physics golden problem (tests/golden/user_cases.npz): inputs and
+    the reference python lane's f64 / f32 outputs for an oracle/user_forms spec."""
+
+    def __init__(self, npz, name):
+        self.name = name
+        meta = json.loads(bytes(npz[f"{name}/meta"]).decode())
+        self.dim, self.spec, self.aux_space = meta["dim"], meta["spec"], meta["aux"]
+        self.n_q, self.n_comp = meta["n_q"], meta["n_comp"]
+        for key in ("basis", "basis_der", "weights", "inv_j", "det_j", "coeffs", "py_f64", "py_f32"):
+            setattr(self, key, npz[f"{name}/{key}"])
+        self.aux = npz[f"{name}/aux"] if f"{name}/aux" in npz.files else None
+
+
+def load_user_cases():
+    npz = np.load(GOLDEN / "user_cases.npz")
+    names = json.loads(bytes(npz["index"]).decode())
+    return [UserCase(npz, n) for n in names]
+
+
+USER_CASES = load_user_cases()

@@ -7,6 +7,9 @@ never runs this: it only reads the committed outputs
 
   tests/golden/small_cases.npz   full inputs + outputs for small problems
   tests/golden/big_hashes.json   sha256 of inputs/outputs for BASELINE configs
+  tests/golden/user_cases.npz    user physics forms (f0, several aux fields,
+                                 grad a; oracle/user_forms.py) through the
+                                 reference's python lane, f64 and f32
 
 Every output here comes from the reference itself:
   * ``ref_f64``  txfem.reference.integrate_reference (reference.py:40-112)
@@ -23,7 +26,7 @@ Input conventions follow the reference tests and CLI:
   * random near-identity Jacobians J = I + 0.2 U(-1,1)
     (tests/test_executor.py:273-280).
 
-Usage:  python tests/golden/make_golden.py
+Usage:  python tests/golden/make_golden.py [user]   (user: only user_cases.npz)
 """
 
 from __future__ import annotations
@@ -220,7 +223,82 @@ def big_hashes():
     return out
 
 
+# ---- user physics (run-time compiled lane) ---------------------------------------
+
+def user_cases():
+    """Every spec of oracle/user_forms.py, built with the REFERENCE's user_form,
+    integrated by the reference's python lane (_kernels_py.integrate_cells,
+    _kernels_py.py:20-110) on inputs cast once to the run dtype."""
+    from txfem import _kernels_py
+    from txfem.physics import user_form as ref_user_form
+
+    sys.path.insert(0, str(REPO))
+    from oracle import user_forms
+
+    arrays, index = {}, []
+    for dim, refine in ((2, 5), (3, 2)):
+        for sname in user_forms.SPECS:
+            spec = user_forms.spec(sname, dim)
+            form = user_forms.make_form(ref_user_form, sname, dim)
+            rng_tab = np.random.default_rng(17 * dim + len(sname))
+            rules = [("q1", *_tables(txfem.quadrature_rule(dim, 1), dim)),
+                     ("q2", *_tables(txfem.two_point_rule(dim), dim)),
+                     ("q3rand", rng_tab.uniform(0, 1, (3, dim + 1)), rng_tab.uniform(-1, 1, (3, dim + 1, dim)),
+                      rng_tab.uniform(0.1, 0.5, 3))]
+            for rname, B, D, W in rules:
+                for family in ("kuhn", "randj"):
+                    seed = 1000 + 100 * dim + 7 * len(index)
+                    pform = FORMS["poisson"][0](dim) if spec["n_comp"] == 1 else FORMS["elasticity"][0](dim)
+                    if family == "kuhn":
+                        mesh = txfem.generate_unit_simplex_mesh(dim, refine)
+                        inv, det, coeffs, _ = kuhn_problem(dim, refine, pform, None, None, seed)
+                        n = mesh.n_cells
+                    else:
+                        n = 61
+                        inv, det, coeffs, _ = randj_problem(dim, n, pform, None, seed)
+                    aux = None
+                    rng = np.random.default_rng(seed + 5)
+                    if spec["aux"] == "p0":
+                        aux = CellAux("p0", rng.uniform(0.5, 1.5, (n, spec["n_aux"])))
+                    elif spec["aux"] == "p1":
+                        if family == "kuhn":
+                            nodal = rng.uniform(0.5, 1.5, (mesh.n_vertices, spec["n_aux"]))
+                            aux = CellAux("p1", np.ascontiguousarray(nodal[mesh.cells]))
+                        else:
+                            aux = CellAux("p1", rng.uniform(0.5, 1.5, (n, dim + 1, spec["n_aux"])))
+                    name = f"{dim}d_{sname}_{rname}_{family}"
+                    index.append(name)
+                    for dt, tag in ((np.float64, "py_f64"), (np.float32, "py_f32")):
+                        c = lambda a: np.ascontiguousarray(a, dtype=dt)  # noqa: E731
+                        out = np.empty((n, dim + 1, spec["n_comp"]), dtype=dt)
+                        ax = None if aux is None else CellAux(aux.space, c(aux.values))
+                        _kernels_py.integrate_cells(form, c(B), c(D), c(W), c(inv), c(det), c(coeffs), ax, out)
+                        arrays[f"{name}/{tag}"] = out
+                    arrays[f"{name}/basis"] = B
+                    arrays[f"{name}/basis_der"] = D
+                    arrays[f"{name}/weights"] = W
+                    arrays[f"{name}/inv_j"] = inv
+                    arrays[f"{name}/det_j"] = det
+                    arrays[f"{name}/coeffs"] = coeffs
+                    if aux is not None:
+                        arrays[f"{name}/aux"] = aux.values
+                    meta = dict(dim=dim, spec=sname, aux=spec["aux"], n_q=int(B.shape[0]), n_comp=spec["n_comp"])
+                    arrays[f"{name}/meta"] = np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8)
+    arrays["index"] = np.frombuffer(json.dumps(index).encode(), dtype=np.uint8)
+    return arrays
+
+
+def _tables(rule, dim):
+    tab = txfem.tabulate(dim, rule)
+    return tab.basis, tab.basis_der, rule.weights
+
+
 def main():
+    if sys.argv[1:] == ["user"]:
+        np.savez_compressed(OUT / "user_cases.npz", **user_cases())
+        print("wrote", OUT / "user_cases.npz")
+        return
+    np.savez_compressed(OUT / "user_cases.npz", **user_cases())
     arrays = small_cases()
     np.savez_compressed(OUT / "small_cases.npz", **arrays)
     (OUT / "big_hashes.json").write_text(json.dumps(big_hashes(), indent=1) + "\n")

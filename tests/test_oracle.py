@@ -92,3 +92,32 @@ def test_reference_lane_from_oracle_ref_matches_golden(case):
                              c(case.weights), c(case.inv_j), c(case.det_j), c(case.coeffs),
                              c(case.aux) if case.aux is not None else None, out)
         assert bitwise_equal(out, getattr(case, key))
+
+
+# ---- user physics: the numpy-lane restatement is pinned to the reference's python lane ----
+from conftest import USER_CASES  # noqa: E402
+
+
+@pytest.mark.parametrize("case", USER_CASES, ids=lambda c: c.name)
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_oracle_forms_bitwise_matches_reference_python_lane(case, dtype):
+    from oracle import user_forms
+
+    s = user_forms.spec(case.spec, case.dim)
+    dt = np.float64 if dtype == "f64" else np.float32
+    out = oracle.integrate_forms(s["f1_many"], s["f0_many"], s["uses_grad_a"], s["aux"], case.basis,
+                                 case.basis_der, case.weights, case.inv_j, case.det_j, case.coeffs, case.aux, dt)
+    assert bitwise_equal(out, case.py_f64 if dtype == "f64" else case.py_f32)
+
+
+def test_oracle_forms_reproduces_shipped_forms():
+    """The generic restatement with the shipped f1 equals the C oracle bit for bit."""
+    import paper_1607_04245_b200 as txb
+
+    for case in SMALL_CASES:
+        factory = {"poisson": txb.poisson_form, "poisson_varcoef": txb.poisson_varcoef_form,
+                   "elasticity": txb.elasticity_form}[case.form]
+        f = factory(case.dim)
+        out = oracle.integrate_forms(f.f1_many, None, False, case.aux_space, case.basis, case.basis_der,
+                                     case.weights, case.inv_j, case.det_j, case.coeffs, case.aux, np.float64)
+        assert bitwise_equal(out, case.ref_f64), case.name

@@ -175,7 +175,7 @@ def rank_workload(name, rank, world, seed=1234):
                 coeffs=c(coeffs), aux=aux, n=hi - lo, dtype=dtype, dim=dim)
 
 
-def time_device(wl, steps, warmup, n_sets, barrier=None, sampler=None):
+def time_device(wl, steps, warmup, n_sets, barrier=None, sampler=None, jit=False):
     """Device-resident timing: K launches rotating over n_sets buffer sets,
     captured in one CUDA graph (so host launch overhead is not timed), bracketed
     by CUDA events on the launching stream.  Falls back to eager launches if
@@ -185,10 +185,11 @@ def time_device(wl, steps, warmup, n_sets, barrier=None, sampler=None):
     from paper_1607_04245_b200 import backend
     from paper_1607_04245_b200.physics import CellAux
 
-    kernel = backend.cuda_kernel(wl["form"], wl["rule"].n_q, wl["aux"], 4 if wl["dtype"] == "f32" else 8)
+    width = 4 if wl["dtype"] == "f32" else 8
+    kernel = (backend.jit_kernel if jit else backend.cuda_kernel)(wl["form"], wl["rule"].n_q, wl["aux"], width)
     sets = []
     for _ in range(n_sets):
-        aux = None if wl["aux"] is None else CellAux("p0", wl["aux"].values.clone())
+        aux = None if wl["aux"] is None else CellAux(wl["aux"].space, wl["aux"].values.clone())
         sets.append((wl["inv"].clone(), wl["det"].clone(), wl["coeffs"].clone(), aux,
                      torch.empty_like(wl["coeffs"])))
     tab, rule = wl["tab"], wl["rule"]
@@ -293,6 +294,57 @@ def time_mesh(name, steps, warmup, n_sets_min=4, given_geometry=False):
     t1.record()
     torch.cuda.synchronize()
     return t0.elapsed_time(t1) / steps, per_cell
+
+
+# A user physics form for the run-time compiled lane's bench rows: two P1
+# auxiliary fields with their gradients and an f0 term (string-injection
+# source, compiled by NVRTC).  Mirrors oracle/user_forms.py "advect".
+_ADVECT_SIG = "(const real u[], const realv gradU[], const real a[], const realv gradA[], int comp)"
+ADVECT_F1 = f"realv f1_advect{_ADVECT_SIG}\n{{\n  return a[0]*gradU[comp] + u[comp]*gradA[1];\n}}\n"
+ADVECT_F0 = f"real f0_advect{_ADVECT_SIG}\n{{\n  return a[1]*u[comp] + dot(gradA[0], gradU[comp]);\n}}\n"
+
+
+def jit_rows(peak, steps):
+    """Run-time compiled lane: the shipped var-coef form through NVRTC (same
+    bytes as the headline) and a user form with f0 + 2 P1 fields + grad a."""
+    import torch
+
+    from paper_1607_04245_b200.perf_model import compulsory_bytes_per_cell
+    from paper_1607_04245_b200.physics import CellAux, user_form
+
+    rows = []
+    for name in ("3d_varcoef_f64", "3d_varcoef_f32"):
+        vf, vb = config_model(name)
+        wl = rank_workload(name, 0, 1)
+        ns = max(4, -(-3 * L2_BYTES // (vb * wl["n"])) + 1)
+        tot, _ = time_device(wl, steps, 5, min(ns, 8), jit=True)
+        ms = tot / steps
+        rows.append({"config": "jit_" + name, "path": "txb_jit_integrate (shipped form's source, NVRTC)",
+                     "dtype": wl["dtype"], "cells": wl["n"], "launch_ms": ms, "gflops": vf * wl["n"] / (ms * 1e-3) / 1e9,
+                     "gbs_launch": vb * wl["n"] / (ms * 1e-3) / 1e9,
+                     "frac": vb * wl["n"] / (ms * 1e-3) / 1e9 / peak, "bytes_per_cell": vb})
+        del wl
+        torch.cuda.empty_cache()
+    for dtype in ("f64", "f32"):
+        base = "3d_varcoef_" + dtype
+        vf, _ = config_model(base)
+        wl = rank_workload(base, 0, 1)
+        n, tdt = wl["n"], wl["coeffs"].dtype
+        wl["form"] = user_form("advect", 3, 1, lambda s, c: None, 9, ADVECT_F1, n_aux=2, f0=lambda s, c: None,
+                               flops_f0=7, source_f0=ADVECT_F0, uses_grad_a=True)
+        wl["aux"] = CellAux("p1", torch.rand((n, 4, 2), dtype=tdt, device="cuda") + 0.5)
+        w = 4 if dtype == "f32" else 8
+        vb = compulsory_bytes_per_cell(3, 1, w, "p1", n_aux=2)
+        ns = max(4, -(-3 * L2_BYTES // (vb * n)) + 1)
+        tot, _ = time_device(wl, steps, 5, min(ns, 8))
+        ms = tot / steps
+        rows.append({"config": "jit_3d_user_advect_" + dtype, "path": "txb_jit_integrate (user form: f0, 2 P1 aux, grad a)",
+                     "dtype": dtype, "cells": n, "launch_ms": ms, "gcells_per_s": n / (ms * 1e-3) / 1e9,
+                     "gbs_launch": vb * n / (ms * 1e-3) / 1e9, "frac": vb * n / (ms * 1e-3) / 1e9 / peak,
+                     "bytes_per_cell": vb})
+        del wl
+        torch.cuda.empty_cache()
+    return rows
 
 
 class _null:
@@ -610,6 +662,7 @@ def main():
                     "gbs": per_cell * n / (ms * 1e-3) / 1e9, "frac": per_cell * n / (ms * 1e-3) / 1e9 / peak})
             torch.cuda.empty_cache()
         variants.extend(mesh_rows)
+        variants.extend(jit_rows(peak, max(50, args.steps // 4)))
         line["variants"] = variants
     print(json.dumps(line), flush=True)
 

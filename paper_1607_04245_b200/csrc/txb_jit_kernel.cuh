@@ -44,6 +44,7 @@ __device__ __forceinline__ int det_bytes(int n) { return round_up(n * S, 16); }
 __device__ __forceinline__ int coef_bytes(int n) { return round_up(n * NBC * S, 16); }
 __device__ __forceinline__ int aux_bytes(int n) { return round_up(n * AUXW * S, 16); }
 
+template <bool VEC>
 __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const real* __restrict__ s_inv,
                                            const real* __restrict__ s_det, const real* __restrict__ s_coef,
                                            const real* __restrict__ s_aux, real* __restrict__ scratch, int c0,
@@ -59,8 +60,9 @@ __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const re
   if (lc < nc) {
     const int cell = c0 + lc;
     real J[DD];
-#pragma unroll
-    for (int m = 0; m < DD; ++m) J[m] = s_inv[cell * DD + m];
+    load_row<real, DD, VEC>(s_inv + cell * DD, J);
+    real cf[NBC];
+    load_row<real, NBC, VEC>(s_coef + cell * NBC, cf);
     const real det = s_det[cell];
 
     // pulled-back gradients T[b][k] = sum_j D[q][b][j] invJ[j][k]  (_kernels_py.py:78-90)
@@ -88,10 +90,9 @@ __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const re
     for (int b = 0; b < NB; ++b)
 #pragma unroll
       for (int c = 0; c < NCOMP; ++c) {
-        const real cf = s_coef[cell * NBC + b * NCOMP + c];
-        u[c] = add(u[c], mul(cf, tab.B[q * NB + b]));
+        u[c] = add(u[c], mul(cf[b * NCOMP + c], tab.B[q * NB + b]));
 #pragma unroll
-        for (int k = 0; k < D; ++k) gradU[c][k] = add(gradU[c][k], mul(cf, tr[b][k]));
+        for (int k = 0; k < D; ++k) gradU[c][k] = add(gradU[c][k], mul(cf[b * NCOMP + c], tr[b][k]));
       }
 
     // auxiliary fields (_kernels_py.py:93-110)
@@ -139,7 +140,7 @@ __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const re
 
   // ------------- basis phase: lane <-> element entry (cell, b, c) -------------
   real* o_base = out + (int64_t)c0 * NBC;
-  for (int o = lane; o < nc * NBC; o += 32) {
+  auto entry = [&](int o) {
     const int ec = o / NBC;
     const int r = o - ec * NBC;
     const int b = r / NCOMP;
@@ -153,6 +154,13 @@ __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const re
         e = add(e, mul(s_tr[ec * TRS + (qq * NB + b) * D + k], s_f1[ec * F1S + (qq * NCOMP + c) * D + k]));
     }
     o_base[o] = e;
+  };
+  constexpr int FULL = CW * NBC;
+  if (nc == CW && FULL % 32 == 0) {
+#pragma unroll
+    for (int i = 0; i < FULL / 32; ++i) entry(i * 32 + lane);  // consecutive lanes, consecutive entries
+  } else {
+    for (int o = lane; o < nc * NBC; o += 32) entry(o);
   }
   __syncwarp();  // scratch is reused by the next slice
 }
@@ -209,12 +217,19 @@ txb_jit_integrate(const __grid_constant__ txb::IntegrateArgs<real> a) {
   real* scratch = reinterpret_cast<real*>(scratch_base + warp * SCRATCH_BYTES);
   pipeline_consume(a, p, smem, stage_bytes, [&](const unsigned char* st, int64_t c0, int ncell) {
     real* out = a.out + c0 * NBC;
-    const real* g_aux = AUXW ? a.aux + c0 * AUXW : nullptr;
-    const real* s_inv = st ? reinterpret_cast<const real*>(st) : a.inv_j + c0 * DD;
-    const real* s_det = st ? reinterpret_cast<const real*>(st + o_det) : a.det_j + c0;
-    const real* s_coef = st ? reinterpret_cast<const real*>(st + o_coef) : a.coeffs + c0 * NBC;
-    const real* s_aux = st ? reinterpret_cast<const real*>(st + o_aux) : g_aux;
-    for (int c = warp * CW; c < ncell; c += W * CW)
-      warp_slice(a.tab, s_inv, s_det, s_coef, s_aux, scratch, c, ncell, out, lane);
+    if (st) {
+      const real* s_inv = reinterpret_cast<const real*>(st);
+      const real* s_det = reinterpret_cast<const real*>(st + o_det);
+      const real* s_coef = reinterpret_cast<const real*>(st + o_coef);
+      const real* s_aux = reinterpret_cast<const real*>(st + o_aux);
+      for (int c = warp * CW; c < ncell; c += W * CW)
+        warp_slice<true>(a.tab, s_inv, s_det, s_coef, s_aux, scratch, c, ncell, out, lane);
+    } else {
+      // unaligned caller buffers or an odd-sized partial batch: straight from global memory
+      const real* g_aux = AUXW ? a.aux + c0 * AUXW : nullptr;
+      for (int c = warp * CW; c < ncell; c += W * CW)
+        warp_slice<false>(a.tab, a.inv_j + c0 * DD, a.det_j + c0, a.coeffs + c0 * NBC, g_aux, scratch, c, ncell,
+                          out, lane);
+    }
   });
 }

@@ -42,28 +42,44 @@ struct IntegrateArgs {
   Tabulation<T> tab;
 };
 
+// 16- and 8-byte vector types per element type (type-preserving: the lanes of
+// the vector ARE elements of the row, no conversion).
+template <typename T> struct Vec16;
+template <> struct Vec16<double> { using type = double2; static constexpr int N = 2; };
+template <> struct Vec16<float> { using type = float4; static constexpr int N = 4; };
+template <> struct Vec16<long> { using type = longlong2; static constexpr int N = 2; };
+template <> struct Vec16<long long> { using type = longlong2; static constexpr int N = 2; };
+template <> struct Vec16<int> { using type = int4; static constexpr int N = 4; };
+template <typename T> struct Vec8;
+template <> struct Vec8<float> { using type = float2; };
+template <> struct Vec8<int> { using type = int2; };
+
+template <typename V, typename T>
+__device__ __forceinline__ void unpack(const V& v, T* r) {
+  r[0] = (T)v.x;
+  r[1] = (T)v.y;
+  if constexpr (sizeof(V) / sizeof(T) == 4) {
+    r[2] = (T)v.z;
+    r[3] = (T)v.w;
+  }
+}
+
 // Vectorised row load: N consecutive T at p (row starts are multiples of
 // N*sizeof(T) from a 16-byte aligned base); widest access the alignment allows.
 template <typename T, int N, bool VEC = true>
 __device__ __forceinline__ void load_row(const T* __restrict__ p, T (&r)[N]) {
   constexpr int BYTES = N * (int)sizeof(T);
-  if constexpr (!VEC) {
+  constexpr bool V16 = VEC && BYTES % 16 == 0;
+  constexpr bool V8 = VEC && !V16 && sizeof(T) == 4 && BYTES % 8 == 0;
+  if constexpr (V16) {
+    using V = typename Vec16<T>::type;
+    constexpr int E = 16 / (int)sizeof(T);
 #pragma unroll
-    for (int i = 0; i < N; ++i) r[i] = p[i];
-  } else if constexpr (BYTES % 16 == 0) {
-    constexpr int V = 16 / sizeof(T);
+    for (int i = 0; i < N; i += E) unpack(*reinterpret_cast<const V*>(p + i), &r[i]);
+  } else if constexpr (V8) {
+    using V = typename Vec8<T>::type;
 #pragma unroll
-    for (int i = 0; i < N; i += V) {
-      const uint4 v = *reinterpret_cast<const uint4*>(p + i);
-      __builtin_memcpy(&r[i], &v, 16);
-    }
-  } else if constexpr (BYTES % 8 == 0) {
-    constexpr int V = 8 / sizeof(T);
-#pragma unroll
-    for (int i = 0; i < N; i += V) {
-      const uint2 v = *reinterpret_cast<const uint2*>(p + i);
-      __builtin_memcpy(&r[i], &v, 8);
-    }
+    for (int i = 0; i < N; i += 2) unpack(*reinterpret_cast<const V*>(p + i), &r[i]);
   } else {
 #pragma unroll
     for (int i = 0; i < N; ++i) r[i] = p[i];

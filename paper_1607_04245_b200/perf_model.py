@@ -89,8 +89,9 @@ def build_estimate(geom: ExecutionGeometry, scalar_width: int = 4, needs_f0: boo
 
 
 def compulsory_bytes_per_cell(dim: int, n_comp: int, scalar_width: int,
-                              aux_space: Optional[str] = None) -> int:
-    """Minimum HBM bytes per cell of one integration pass (see module doc)."""
+                              aux_space: Optional[str] = None, n_aux: int = 1) -> int:
+    """Minimum HBM bytes per cell of one integration pass (see module doc);
+    ``n_aux`` auxiliary fields per point (run-time compiled forms)."""
     n_b = dim + 1
-    aux = 0 if aux_space is None else (1 if aux_space == "p0" else n_b)
+    aux = 0 if aux_space is None else (n_aux if aux_space == "p0" else n_b * n_aux)
     return scalar_width * (dim * dim + 1 + n_b * n_comp + aux + n_b * n_comp)

@@ -36,7 +36,7 @@ from .schedule import DEFAULT_THREAD_LIMIT, ExecutionGeometry, derive_execution_
 from .trace import ChunkTrace, ExecutionTrace, model_batch_counters, shared_image_bytes
 
 __all__ = ["DEFAULT_SHARED_MEM_LIMIT", "scalar_dtype", "execute_chunk", "integrate_transposed",
-           "integrate_cells", "integrate_mesh"]
+           "integrate_cells", "integrate_mesh", "integrate_partitioned"]
 
 DEFAULT_SHARED_MEM_LIMIT = 48 * 1024
 _DTYPE_NAMES = {"f32": np.float32, "f64": np.float64}
@@ -272,3 +272,45 @@ def integrate_mesh(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: Quadr
         if i >= 0:
             raise OrientationError(f"cell {i} is degenerate or negatively oriented")
     return res
+
+
+def integrate_partitioned(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: QuadratureRule,
+                          form: PhysicsForm, coeffs_global, aux: Optional[CellAux] = None, *, rank: int,
+                          world: int, exchange=None, dtype="f64", plan=None, align: int = 256, n_bl: int = 0):
+    """One rank's share of integrate_transposed for the contiguous cell-range
+    partition over ``world`` ranks (shard.cell_range): integrate the rank's
+    cells on its GPU, then the halo exchange + assembly of halo.py.
+
+    Returns (owned_vertex_ids (numpy), owned_residual (CUDA tensor
+    (n_owned * n_comp,)), plan).  Concatenating every rank's owned entries
+    reproduces the reference residual (executor.py:266, np.add.at order) bit
+    for bit.  ``exchange``: halo.all_to_all_exchange() under torch.distributed
+    (None for world == 1).  ``plan``: a cached halo.build_halo_plan result."""
+    from . import halo
+
+    torch = _torch()
+    dt = scalar_dtype(dtype)
+    form.require_aux(aux)
+    if plan is None:
+        plan = halo.build_halo_plan(mesh.cells, mesh.n_vertices, rank, world, align)
+    lo, hi = plan.lo, plan.hi
+    n_b, nc = tab.n_b, form.n_comp
+    sub = Mesh(mesh.dim, mesh.vertices, np.ascontiguousarray(mesh.cells[lo:hi]))
+    tdt = torch.float32 if dt == np.float32 else torch.float64
+    buf = torch.empty((plan.n_local_rows + plan.n_recv, nc), dtype=tdt, device="cuda")
+    elem = buf[:plan.n_local_rows].view(hi - lo, n_b, nc)
+    if hi > lo:
+        kernel = _resolve_backend(None, form, rule.n_q, aux, dt.itemsize)
+        glob_dev = _dev(coeffs_global, torch, dt)
+        aux_dev = None if aux is None else CellAux(aux.space, _dev(aux.values[lo:hi], torch, dt))
+        cells_dev = torch.from_numpy(sub.cells.astype(np.int64)).to("cuda")
+        if _mesh_fusable(tab, rule) and not isinstance(kernel, _backend.JitKernel):
+            integrate_mesh(sub, layout, tab, rule, form, glob_dev, aux_dev, dtype=dt, cells=cells_dev, out=elem,
+                           n_bl=n_bl)
+        else:
+            g = compute_geometry(sub, cells=cells_dev, device_out=True)
+            blocks = gather_coefficients(sub, layout, glob_dev, cells=cells_dev)
+            integrate_cells(tab, rule, CellGeometry(_dev(g.inv_jacobians, torch, dt), _dev(g.determinants, torch, dt)),
+                            blocks, aux_dev, form, dtype=dt, out=elem, n_bl=n_bl)
+    owned = halo.assemble_owned(plan, buf, nc, exchange)
+    return plan.owned, owned.reshape(-1), plan

@@ -1,0 +1,165 @@
+"""Partitioned global assembly with a halo exchange (paper_1607_04245_b200/halo.py).
+
+CPU: plan invariants; world_size 2 and 3 over gloo with the oracle standing
+in for the device (element vectors, row gather, CSR chain) and the REAL
+all_to_all_single exchange — the gathered owned residuals equal the
+reference's np.add.at residual over the whole mesh bit for bit.
+GPU: the device path (integration + pack kernel + scatter kernel) for several
+emulated ranks in one process (a mailbox stands in for the collective; ranks
+run from the highest down, since rank r only receives from ranks above it)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import bitwise_equal
+from oracle import oracle
+from paper_1607_04245_b200 import halo
+from paper_1607_04245_b200.mesh import generate_unit_simplex_mesh
+from paper_1607_04245_b200.shard import all_ranges
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def chain_assemble(plan, buf):
+    """The CSR chain txb_scatter_add runs: per owned vertex, +0 then each row in order."""
+    counts = np.diff(plan.offsets)
+    out = np.zeros((plan.owned.size, buf.shape[1]), dtype=buf.dtype)
+    for j in range(int(counts.max()) if counts.size else 0):
+        live = np.nonzero(counts > j)[0]
+        out[live] += buf[plan.incidence[plan.offsets[live] + j]]
+    return out
+
+
+@pytest.mark.parametrize("dim,refine,world,align", [(2, 12, 2, 16), (2, 12, 3, 16), (3, 4, 4, 16), (3, 4, 8, 1),
+                                                    (3, 3, 5, 64), (2, 3, 4, 256)])
+def test_plan_partitions_every_contribution(dim, refine, world, align):
+    mesh = generate_unit_simplex_mesh(dim, refine)
+    n, n_b = mesh.cells.shape
+    owner = halo.vertex_owners(mesh.cells, mesh.n_vertices, world, align)
+    plans = [halo.build_halo_plan(mesh.cells, mesh.n_vertices, r, world, align, owner) for r in range(world)]
+    owned = np.concatenate([p.owned for p in plans])
+    assert np.array_equal(np.sort(owned), np.unique(mesh.cells))  # each touched vertex owned exactly once
+    assert sum(p.offsets[-1] for p in plans) == n * n_b          # every incidence contributes exactly once
+    for r, p in enumerate(plans):
+        assert (p.lo, p.hi) == all_ranges(n, world, align)[r]
+        for s in range(world):  # what r sends to s is what s expects from r
+            assert p.send_counts[s] == plans[s].recv_counts[r]
+        assert all(p.send_counts[s] == 0 for s in range(r, world))
+        assert all(p.recv_counts[s] == 0 for s in range(0, r + 1))
+        assert p.incidence.dtype == np.int32 and p.incidence.max(initial=-1) < p.n_local_rows + p.n_recv
+
+
+def _elem(mesh, lo, hi):
+    inv, det = oracle.geometry(mesh.vertices, mesh.cells[lo:hi])
+    glob = np.random.default_rng(5).standard_normal(mesh.n_vertices)
+    co = oracle.gather(mesh.cells[lo:hi], glob, 1)
+    kappa = np.random.default_rng(6).uniform(0.5, 1.5, (mesh.n_cells, 1))[lo:hi]
+    B, D, W = oracle.p1_tables(mesh.dim)
+    return oracle.integrate(1, 1, B, D, W, inv, det, co, kappa, np.float64)
+
+
+def _worker(rank, world, port, dim, refine, align, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mesh = generate_unit_simplex_mesh(dim, refine)
+        plan = halo.build_halo_plan(mesh.cells, mesh.n_vertices, rank, world, align)
+        buf = np.zeros((plan.n_local_rows + plan.n_recv, 1))
+        buf[:plan.n_local_rows] = _elem(mesh, plan.lo, plan.hi).reshape(-1, 1)
+        send = torch.from_numpy(np.ascontiguousarray(buf[plan.send_rows]).reshape(-1))
+        recv = torch.zeros(plan.n_recv, dtype=torch.float64)
+        halo.all_to_all_exchange()(recv, send, plan.recv_counts, plan.send_counts)
+        buf[plan.n_local_rows:, 0] = recv.numpy()
+        parts = [None] * world
+        dist.all_gather_object(parts, (plan.owned, chain_assemble(plan, buf)))
+        if rank == 0:
+            glob = np.zeros(mesh.n_vertices)
+            for ids, vals in parts:
+                glob[ids] = vals[:, 0]
+            q.put(glob.tobytes())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dim,refine,world,align", [(2, 10, 2, 16), (3, 3, 3, 16)])
+def test_gloo_halo_exchange_reproduces_reference_residual(dim, refine, world, align):
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    procs = mp.start_processes(_worker, args=(world, _free_port(), dim, refine, align, q), nprocs=world,
+                               start_method="spawn", join=False)
+    blob = q.get()
+    while not procs.join(timeout=60):
+        pass
+    mesh = generate_unit_simplex_mesh(dim, refine)
+    ref = oracle.scatter_add(mesh.cells, _elem(mesh, 0, mesh.n_cells), mesh.n_vertices)
+    assert blob == ref.tobytes()
+
+
+# ------------------------------------------------------------------ GPU ----
+
+class Mailbox:
+    def __init__(self):
+        self.box = {}
+
+    def exchange_for(self, rank, plan):
+        def ex(recv, send, recv_splits, send_splits):
+            o = 0
+            for p, c in enumerate(send_splits):
+                if c:
+                    self.box[(rank, p)] = send[o:o + c].clone()
+                o += c
+            o = 0
+            for s, c in enumerate(recv_splits):
+                if c:
+                    recv[o:o + c].copy_(self.box.pop((s, rank)))
+                o += c
+        return ex
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,align", [(1, 256), (2, 256), (3, 64), (8, 16)])
+@pytest.mark.parametrize("physics", ["varcoef_p0", "elasticity"])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_partitioned_integration_equals_reference_residual(world, align, physics, dtype):
+    import paper_1607_04245_b200 as txb
+
+    dim = 3
+    mesh = txb.generate_unit_simplex_mesh(dim, 9)
+    form = txb.poisson_varcoef_form(dim) if physics == "varcoef_p0" else txb.elasticity_form(dim)
+    layout = txb.FieldLayout(form.n_comp)
+    rule = txb.quadrature_rule(dim, 1)
+    tab = txb.tabulate(dim, rule)
+    glob = np.random.default_rng(1).standard_normal(layout.global_size(mesh))
+    aux = None
+    if form.n_aux:
+        aux = txb.CellAux("p0", np.random.default_rng(2).uniform(0.5, 1.5, (mesh.n_cells, 1)))
+    npdt = np.float64 if dtype == "f64" else np.float32
+    mb = Mailbox()
+    got = np.zeros(layout.global_size(mesh), dtype=npdt)
+    for r in reversed(range(world)):
+        plan = halo.build_halo_plan(mesh.cells, mesh.n_vertices, r, world, align)
+        ids, res, _ = txb.integrate_partitioned(mesh, layout, tab, rule, form, glob, aux, rank=r, world=world,
+                                                exchange=mb.exchange_for(r, plan), dtype=dtype, plan=plan)
+        torch.cuda.synchronize()
+        got.reshape(-1, form.n_comp)[ids] = res.cpu().numpy().reshape(-1, form.n_comp)
+    assert not mb.box
+    # reference: every cell integrated, then np.add.at over the whole mesh (executor.py:266)
+    inv, det = oracle.geometry(mesh.vertices, mesh.cells)
+    co = oracle.gather(mesh.cells, glob, form.n_comp)
+    fc = 1 if physics == "varcoef_p0" else 2
+    elem = oracle.integrate(fc, 1 if aux is not None else 0, tab.basis, tab.basis_der, rule.weights, inv, det,
+                            co, None if aux is None else aux.values, npdt)
+    want = oracle.scatter_add(mesh.cells, elem, mesh.n_vertices)
+    assert bitwise_equal(got, want)

@@ -424,15 +424,18 @@ int integrate_device(const Config& c, int n_b, int64_t n_cells, const void* basi
 }
 
 // ---------------------------------------------------------------------------
-// Host-buffer path: pieces of cells pipelined over two streams
-// (H2D of piece p+1 overlaps the kernel of p and the D2H of p-1).
+// Host-buffer path: pieces of cells pipelined over NS streams (slots); the
+// H2D of piece p+1.. overlaps the kernel and the D2H of earlier pieces, so the
+// H2D copy engine (the PCIe-bound resource: inputs are 3.7x the output bytes)
+// stays busy.  Small pieces shorten the pipeline fill and drain.
 // ---------------------------------------------------------------------------
+constexpr int HOST_MAX_SLOTS = 4;
+
 struct HostPathState {
   int device = -1;
   size_t cap = 0;
-  unsigned char* buf[2] = {nullptr, nullptr};
-  cudaStream_t streams[2] = {nullptr, nullptr};
-  cudaEvent_t done[2] = {nullptr, nullptr};
+  unsigned char* buf[HOST_MAX_SLOTS] = {};
+  cudaStream_t streams[HOST_MAX_SLOTS] = {};
 };
 
 static std::mutex g_host_mu;
@@ -442,18 +445,16 @@ static int host_state(int dev, size_t need, HostPathState*& out) {
   if ((int)g_host_state.size() <= dev) g_host_state.resize(dev + 1);
   HostPathState& s = g_host_state[dev];
   if (!s.streams[0]) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < HOST_MAX_SLOTS; ++i)
       TXB_CUDA_TRY(cudaStreamCreateWithFlags(&s.streams[i], cudaStreamNonBlocking));
-      TXB_CUDA_TRY(cudaEventCreateWithFlags(&s.done[i], cudaEventDisableTiming));
-    }
   }
   if (s.cap < need) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < HOST_MAX_SLOTS; ++i) {
       if (s.buf[i]) cudaFree(s.buf[i]);
       s.buf[i] = nullptr;
     }
     s.cap = 0;
-    for (int i = 0; i < 2; ++i) TXB_CUDA_TRY(cudaMalloc(&s.buf[i], need));
+    for (int i = 0; i < HOST_MAX_SLOTS; ++i) TXB_CUDA_TRY(cudaMalloc(&s.buf[i], need));
     s.cap = need;
   }
   s.device = dev;
@@ -479,8 +480,10 @@ int integrate_host(const Config& c, int n_b, int64_t n_cells, const void* basis,
                                (int64_t)auxw * s, (int64_t)nb * c.n_comp * s};
   int64_t cell_bytes = 0;
   for (int64_t v : per_cell) cell_bytes += v;
-  // Pieces of ~32 MiB (multiple of 64 cells, keeps every slice 16B aligned).
-  int64_t piece = std::max<int64_t>(64, ((int64_t)32 << 20) / cell_bytes);
+  // Pieces of ~TXB_HOST_PIECE_MB MiB (multiple of 64 cells, keeps every slice 16B aligned).
+  const int64_t piece_bytes = (int64_t)std::max(1, env_int("TXB_HOST_PIECE_MB", 32)) << 20;
+  const int slots = std::min(HOST_MAX_SLOTS, std::max(2, env_int("TXB_HOST_SLOTS", 2)));
+  int64_t piece = std::max<int64_t>(64, piece_bytes / cell_bytes);
   piece = (piece + 63) / 64 * 64;
   piece = std::min<int64_t>(piece, (n_cells + 63) / 64 * 64);
   size_t need = 0;
@@ -497,7 +500,7 @@ int integrate_host(const Config& c, int n_b, int64_t n_cells, const void* basis,
                                  (const unsigned char*)coeffs, (const unsigned char*)aux};
   int64_t p = 0;
   for (int64_t c0 = 0; c0 < n_cells; c0 += piece, ++p) {
-    const int slot = (int)(p & 1);
+    const int slot = (int)(p % slots);
     cudaStream_t sm = st->streams[slot];
     const int64_t n = std::min(piece, n_cells - c0);
     unsigned char* base = st->buf[slot];
@@ -517,7 +520,7 @@ int integrate_host(const Config& c, int n_b, int64_t n_cells, const void* basis,
     TXB_CUDA_TRY(cudaMemcpyAsync((unsigned char*)out + c0 * per_cell[4], dptr[4], n * per_cell[4],
                                  cudaMemcpyDeviceToHost, sm));
   }
-  for (int i = 0; i < 2; ++i) TXB_CUDA_TRY(cudaStreamSynchronize(st->streams[i]));
+  for (int i = 0; i < slots; ++i) TXB_CUDA_TRY(cudaStreamSynchronize(st->streams[i]));
   return TXB_OK;
 }
 

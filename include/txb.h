@@ -199,6 +199,12 @@ int txb_jit_integrate(void* kernel, int64_t n_cells, const void* basis, const vo
                       const void* weights, const void* inv_j, const void* det_j, const void* coeffs,
                       const void* aux, void* out, int n_bl, int n_cb, void* stream);
 
+/* Debug timeline of txb_integrate_cells launches made by THIS thread: each
+ * later launch takes the next 4*grid u64 of `device_buf` (capacity in u64) and
+ * its CTAs write %globaltimer stamps [entry, after the previous-grid wait,
+ * first batch ready, consumers done].  NULL turns it off.  Tuning aid only. */
+int txb_debug_trace(void* device_buf, int64_t capacity_u64);
+
 /* STREAM-like probe at a given read:write byte ratio (device pointers):
  * reads `read_bytes` from src, writes `write_bytes` to dst, 16-byte vector
  * accesses.  Used by bench.py for the "measured achievable" bandwidth. */

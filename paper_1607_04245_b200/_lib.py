@@ -39,6 +39,7 @@ SIGNATURES = {
     "txb_build_incidence": (_I, [c_int64, _I, c_int64, _P, _P, _P, _P, _P]),
     "txb_compute_geometry": (_I, [_I, c_int64, _P, _P, _P, _P, POINTER(c_int64), _P]),
     "txb_stream_probe": (_I, [_P, c_int64, _P, c_int64, _P]),
+    "txb_debug_trace": (_I, [_P, c_int64]),
     "txb_jit_compile": (_I, [c_char_p, c_char_p, c_char_p, _I, _I, _I, _I, _I, _I, _I, POINTER(c_void_p)]),
     "txb_jit_source": (c_char_p, [_P]),
     "txb_jit_log": (c_char_p, [_P]),

@@ -211,6 +211,7 @@ integrate_kernel(const __grid_constant__ IntegrateArgs<T> a) {
   const int nbc = a.n_bc;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int W = a.warps;
+  if (threadIdx.x == 0) trace_stamp(a.trace, 0);
   const int stage_bytes = L::stage_bytes(nbc);
   unsigned char* scratch_base = smem + a.stages * stage_bytes;
   const PipelineSmem p = carve_pipeline(scratch_base + W * S::BYTES);
@@ -228,6 +229,7 @@ integrate_kernel(const __grid_constant__ IntegrateArgs<T> a) {
     });
   }
   pipeline_wait_prior_grid();
+  if (threadIdx.x == 0) trace_stamp(a.trace, 1);
 
   if (warp == W) {
     // ============================ producer warp ============================
@@ -254,7 +256,10 @@ integrate_kernel(const __grid_constant__ IntegrateArgs<T> a) {
 
   // ============================ consumer warps ============================
   unsigned char* scratch = scratch_base + warp * S::BYTES;
+  bool first = true;
   pipeline_consume(a, p, smem, stage_bytes, [&](const unsigned char* st, int64_t c0, int ncell) {
+    if (first && threadIdx.x == 0) trace_stamp(a.trace, 2);
+    first = false;
     T* out = a.out + c0 * NBC;
     if (st) {
       const T* s_inv = reinterpret_cast<const T*>(st);
@@ -273,6 +278,7 @@ integrate_kernel(const __grid_constant__ IntegrateArgs<T> a) {
                                                           lane);
     }
   });
+  if (threadIdx.x == 0) trace_stamp(a.trace, 3);
 }
 
 // ---------------------------------------------------------------------------
@@ -372,6 +378,7 @@ static int launch_t(const Config& c, const KernelInfo& k, const Geometry& g, int
            sized16(1) && sized16(nb * c.n_comp) && (c.aux == 0 || sized16(auxw)) &&
            env_int("TXB_DISABLE_BULK", 0) == 0;
   a.prefetch = prefetch_batches(g);
+  a.trace = next_trace_slot(g.grid);
   fill_tab(a.tab, c.n_q, c.dim + 1, c.dim, basis, basis_der, weights);
   void* params[] = {&a};
   cudaLaunchConfig_t cfg = {};
@@ -606,6 +613,11 @@ extern "C" int txb_integrate_cells_host(int form_code, int aux_mode, int dtype_b
   Config c{form_code, aux_mode, dtype_bytes, dim, n_q, n_comp};
   return integrate_host(c, n_b, n_cells, basis, basis_der, weights, inv_j, det_j, coeffs, aux, out,
                         n_bl, n_cb);
+}
+
+extern "C" int txb_debug_trace(void* device_buf, int64_t capacity_u64) {
+  set_trace_buffer((unsigned long long*)device_buf, capacity_u64);
+  return TXB_OK;
 }
 
 extern "C" int txb_stream_probe(const void* src, int64_t read_bytes, void* dst,

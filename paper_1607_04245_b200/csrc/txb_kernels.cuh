@@ -339,6 +339,27 @@ static unsigned long long* work_pool_base() {
   return cache[dev];
 }
 
+// Debug timeline (txb_debug_trace): consecutive launches on this thread take
+// consecutive slots of 4 stamps per CTA from the installed device buffer.
+struct TraceState {
+  unsigned long long* buf = nullptr;
+  int64_t cap = 0, used = 0;
+};
+static thread_local TraceState g_trace;
+
+static void set_trace_buffer(unsigned long long* buf, int64_t cap) {
+  g_trace.buf = buf;
+  g_trace.cap = buf ? cap : 0;
+  g_trace.used = 0;
+}
+
+static unsigned long long* next_trace_slot(int grid) {
+  if (!g_trace.buf || g_trace.used + 4 * (int64_t)grid > g_trace.cap) return nullptr;
+  unsigned long long* p = g_trace.buf + g_trace.used;
+  g_trace.used += 4 * (int64_t)grid;
+  return p;
+}
+
 // Batches per CTA to warm into L2 before the programmatic-launch wait
 // (TXB_PREFETCH_BATCHES; default: the ring depth).
 static int prefetch_batches(const Geometry& g) {

@@ -39,6 +39,7 @@ struct IntegrateArgs {
   unsigned long long* work;  // dynamic mode: {next batch, CTAs done}, self-resetting; NULL = static chunks
   int64_t static_batches;    // dynamic mode: batches dealt round-robin before the counter takes over
   int prefetch;              // batches per CTA warmed into L2 before the programmatic-launch wait
+  unsigned long long* trace; // debug (txb_debug_trace): 4 %globaltimer stamps per CTA, NULL = off
   Tabulation<T> tab;
 };
 
@@ -148,6 +149,18 @@ __device__ __forceinline__ void pipeline_first_batches(const Args& a, int count,
     const int64_t hi = min(a.n_cells, lo + a.chunk_cells);
     for (int64_t c0 = lo; count > 0 && c0 < hi; c0 += nbc, --count) f(c0, (int)min((int64_t)nbc, hi - c0));
   }
+}
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Debug timeline (txb_debug_trace): per CTA [entry, after the grid-dependency
+// wait, first batch ready in consumer warp 0, consumer warp 0 done].
+__device__ __forceinline__ void trace_stamp(unsigned long long* trace, int k) {
+  if (trace) trace[blockIdx.x * 4 + k] = global_ns();
 }
 
 // Programmatic dependent launch: everything before this overlapped the

@@ -53,7 +53,7 @@ CONFIGS = {
 }
 HEADLINE = "3d_varcoef_f64"
 VARIANTS = ["3d_varcoef_f32", "2d_varcoef_f64", "2d_varcoef_f32", "2d_elasticity_f64", "2d_elasticity_f32",
-            "3d_elasticity_f64", "3d_elasticity_f32", "3d_varcoef_f32_2^24", "3d_varcoef_f64_2^24"]
+            "3d_elasticity_f64", "3d_elasticity_f32"]
 
 
 def peaks():
@@ -302,6 +302,40 @@ def time_mesh(name, steps, warmup, n_sets_min=4, given_geometry=False):
 _ADVECT_SIG = "(const real u[], const realv gradU[], const real a[], const realv gradA[], int comp)"
 ADVECT_F1 = f"realv f1_advect{_ADVECT_SIG}\n{{\n  return a[0]*gradU[comp] + u[comp]*gradA[1];\n}}\n"
 ADVECT_F0 = f"real f0_advect{_ADVECT_SIG}\n{{\n  return a[1]*u[comp] + dot(gradA[0], gradU[comp]);\n}}\n"
+
+
+def sweep_rows(peak):
+    """BASELINE.json configs[4]: 3D P1 var-coef Laplacian at 2^24..2^27 cells on
+    one GPU, f32 and f64.  The 2^20-cell Kuhn workload is tiled on the device
+    (cells are independent; values do not affect timing).  Every size is larger
+    than L2, so one buffer set; 10 graph-captured launches (5 at 2^27)."""
+    import torch
+
+    rows = []
+    for dtype in ("f32", "f64"):
+        base = "3d_varcoef_" + dtype
+        vf, vb = config_model(base)
+        wl = rank_workload(base, 0, 1)
+        for lg in (24, 25, 26, 27):
+            reps = 1 << (lg - 20)
+            big = dict(wl, n=wl["n"] * reps, inv=wl["inv"].repeat(reps, 1, 1), det=wl["det"].repeat(reps),
+                       coeffs=wl["coeffs"].repeat(reps, 1, 1))
+            from paper_1607_04245_b200.physics import CellAux
+
+            big["aux"] = CellAux("p0", wl["aux"].values.repeat(reps, 1))
+            steps = 10 if lg < 27 else 5
+            tot, _ = time_device(big, steps, 3, 1)
+            ms = tot / steps
+            rows.append({"config": f"3d_varcoef_{dtype}_2^{lg}", "dtype": dtype, "cells": big["n"],
+                         "launch_ms": ms, "gflops": vf * big["n"] / (ms * 1e-3) / 1e9,
+                         "gbs_launch": vb * big["n"] / (ms * 1e-3) / 1e9,
+                         "frac": vb * big["n"] / (ms * 1e-3) / 1e9 / peak, "bytes_per_cell": vb,
+                         "data": "2^20-cell Kuhn workload tiled on the device; one set (> L2)"})
+            del big
+            torch.cuda.empty_cache()
+        del wl
+        torch.cuda.empty_cache()
+    return rows
 
 
 def jit_rows(peak, steps):
@@ -662,6 +696,7 @@ def main():
                     "gbs": per_cell * n / (ms * 1e-3) / 1e9, "frac": per_cell * n / (ms * 1e-3) / 1e9 / peak})
             torch.cuda.empty_cache()
         variants.extend(mesh_rows)
+        variants.extend(sweep_rows(peak))
         variants.extend(jit_rows(peak, max(50, args.steps // 4)))
         line["variants"] = variants
     print(json.dumps(line), flush=True)

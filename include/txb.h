@@ -202,7 +202,8 @@ int txb_jit_integrate(void* kernel, int64_t n_cells, const void* basis, const vo
 /* Debug timeline of txb_integrate_cells launches made by THIS thread: each
  * later launch takes the next 4*grid u64 of `device_buf` (capacity in u64) and
  * its CTAs write %globaltimer stamps [entry, after the previous-grid wait,
- * first batch ready, consumers done].  NULL turns it off.  Tuning aid only. */
+ * first batch ready (only in builds with -DTXB_TRACE_FIRST_BATCH, else 0),
+ * consumers done].  NULL turns it off.  Tuning aid only. */
 int txb_debug_trace(void* device_buf, int64_t capacity_u64);
 
 /* STREAM-like probe at a given read:write byte ratio (device pointers):

@@ -256,10 +256,14 @@ integrate_kernel(const __grid_constant__ IntegrateArgs<T> a) {
 
   // ============================ consumer warps ============================
   unsigned char* scratch = scratch_base + warp * S::BYTES;
+#ifdef TXB_TRACE_FIRST_BATCH  // costs registers in the consumer loop: tuning builds only
   bool first = true;
+#endif
   pipeline_consume(a, p, smem, stage_bytes, [&](const unsigned char* st, int64_t c0, int ncell) {
+#ifdef TXB_TRACE_FIRST_BATCH
     if (first && threadIdx.x == 0) trace_stamp(a.trace, 2);
     first = false;
+#endif
     T* out = a.out + c0 * NBC;
     if (st) {
       const T* s_inv = reinterpret_cast<const T*>(st);

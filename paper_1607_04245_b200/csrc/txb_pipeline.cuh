@@ -55,16 +55,6 @@ template <typename T> struct Vec8;
 template <> struct Vec8<float> { using type = float2; };
 template <> struct Vec8<int> { using type = int2; };
 
-template <typename V, typename T>
-__device__ __forceinline__ void unpack(const V& v, T* r) {
-  r[0] = (T)v.x;
-  r[1] = (T)v.y;
-  if constexpr (sizeof(V) / sizeof(T) == 4) {
-    r[2] = (T)v.z;
-    r[3] = (T)v.w;
-  }
-}
-
 // Vectorised row load: N consecutive T at p (row starts are multiples of
 // N*sizeof(T) from a 16-byte aligned base); widest access the alignment allows.
 template <typename T, int N, bool VEC = true>
@@ -76,11 +66,23 @@ __device__ __forceinline__ void load_row(const T* __restrict__ p, T (&r)[N]) {
     using V = typename Vec16<T>::type;
     constexpr int E = 16 / (int)sizeof(T);
 #pragma unroll
-    for (int i = 0; i < N; i += E) unpack(*reinterpret_cast<const V*>(p + i), &r[i]);
+    for (int i = 0; i < N; i += E) {
+      const V v = *reinterpret_cast<const V*>(p + i);
+      r[i] = (T)v.x;
+      r[i + 1] = (T)v.y;
+      if constexpr (E == 4) {
+        r[i + 2] = (T)v.z;
+        r[i + 3] = (T)v.w;
+      }
+    }
   } else if constexpr (V8) {
     using V = typename Vec8<T>::type;
 #pragma unroll
-    for (int i = 0; i < N; i += 2) unpack(*reinterpret_cast<const V*>(p + i), &r[i]);
+    for (int i = 0; i < N; i += 2) {
+      const V v = *reinterpret_cast<const V*>(p + i);
+      r[i] = (T)v.x;
+      r[i + 1] = (T)v.y;
+    }
   } else {
 #pragma unroll
     for (int i = 0; i < N; ++i) r[i] = p[i];

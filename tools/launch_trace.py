@@ -3,7 +3,9 @@
 
 python tools/launch_trace.py [config] [launches]
 Each launch's CTAs stamp %globaltimer at entry, after griddepcontrol.wait, at
-their first ready batch and when their consumers finish (txb_debug_trace).
+their first ready batch (libtxb built with NVCC_EXTRA=-DTXB_TRACE_FIRST_BATCH
+only; the stamp costs registers) and when their consumers finish
+(txb_debug_trace).
 """
 import json
 import sys

@@ -8,6 +8,15 @@
 
 namespace txb {
 
+// Stage release: every consumer lane arrives on the stage's `empty` barrier
+// (1), or lane 0 alone after __syncwarp (0).  Both are race-free by the PTX
+// memory model; (1) does not rely on __syncwarp's memory ordering and is the
+// form compute-sanitizer racecheck verifies clean (profiles/r1_sanitizer.md).
+#ifndef TXB_EMPTY_ARRIVE_ALL
+#define TXB_EMPTY_ARRIVE_ALL 1
+#endif
+constexpr int EMPTY_ARRIVALS_PER_WARP = TXB_EMPTY_ARRIVE_ALL ? 32 : 1;
+
 constexpr int MAX_D = TXB_MAX_DIM, MAX_B = TXB_MAX_BASIS, MAX_Q = TXB_MAX_QUAD;
 constexpr int MAX_CONSUMER_WARPS = 16;
 constexpr int MAX_STAGES = 8;
@@ -129,7 +138,7 @@ __device__ __forceinline__ void pipeline_init(const Args& a, const PipelineSmem&
     *p.warps_done = 0;
     for (int s = 0; s < a.stages; ++s) {
       mbar_init(&p.full[s], 1);
-      mbar_init(&p.empty[s], a.warps);
+      mbar_init(&p.empty[s], a.warps * EMPTY_ARRIVALS_PER_WARP);
     }
     fence_mbar_init();
   }
@@ -238,8 +247,12 @@ __device__ __forceinline__ void pipeline_consume(const Args& a, const PipelineSm
       consume(stages + stage * stage_bytes, c0, nsig);
     else
       consume(nullptr, c0, -nsig);
-    __syncwarp();
+#if TXB_EMPTY_ARRIVE_ALL
+    mbar_arrive(&p.empty[stage]);  // every lane releases its own reads of the stage
+#else
+    __syncwarp();  // orders the other lanes' reads of the stage before lane 0's release
     if (lane == 0) mbar_arrive(&p.empty[stage]);
+#endif
     if (++stage == a.stages) {
       stage = 0;
       phase ^= 1;

@@ -53,7 +53,7 @@ CONFIGS = {
 }
 HEADLINE = "3d_varcoef_f64"
 VARIANTS = ["3d_varcoef_f32", "2d_varcoef_f64", "2d_varcoef_f32", "2d_elasticity_f64", "2d_elasticity_f32",
-            "3d_elasticity_f64", "3d_elasticity_f32"]
+            "3d_elasticity_f64", "3d_elasticity_f32", "2d_varcoef_f64_65536"]
 
 
 def peaks():

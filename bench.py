@@ -672,7 +672,7 @@ def main():
             vw = rank_workload(v, 0, 1)
             vs = max(4, -(-3 * L2_BYTES // (vb * vw["n"])) + 1)
             steps = max(50, args.steps // 4) if vw["n"] <= (1 << 20) else 40
-            tot, _ = time_device(vw, steps, 5, min(vs, 8))
+            tot, _ = time_device(vw, steps, 5, min(vs, 64))  # sets x bytes > 3x L2
             vl = tot / steps
             variants.append({"config": v, "dtype": vw["dtype"], "cells": vw["n"],
                              "gflops": vf * vw["n"] / (tot / steps * 1e-3) / 1e9,

@@ -24,6 +24,9 @@
  *                             txfem/codegen.py:50-256 generate_kernel_source,
  *                             executed by the python lane
  *                             txfem/_kernels_py.py:20-110 (f0, n_aux, grad a)
+ *   txb_halo_*             <- the global assembly across partitions (executor.py:266,
+ *                             mesh.py:220-234 np.add.at order) for cell-range
+ *                             partitions: peer-memory pack-and-put + assembly
  *   txb_last_error         error text for the Python exception message
  *
  * Codes follow the reference (backend.py:26-27):
@@ -198,6 +201,37 @@ int64_t txb_jit_cubin(void* kernel, void* dst, int64_t capacity);
 int txb_jit_integrate(void* kernel, int64_t n_cells, const void* basis, const void* basis_der,
                       const void* weights, const void* inv_j, const void* det_j, const void* coeffs,
                       const void* aux, void* out, int n_bl, int n_cb, void* stream);
+
+/* ---- Halo exchange over peer memory (one node, NVLink / NVSwitch) --------
+ * The global-residual exchange of halo.py without NCCL: every rank exposes a
+ * WINDOW (header of epoch flags/acks + two receive slots of n_recv rows), shared
+ * with the other processes by CUDA IPC handle (64 bytes).  Per residual
+ * evaluation (epoch 1, 2, ...):
+ *   txb_halo_put       stores this rank's owed rows straight into each owner's
+ *                      window (P2P), then publishes the epoch in the owners'
+ *                      flags (release, system scope); waits for the owner's ack
+ *                      of epoch-2 before reusing a slot;
+ *   txb_halo_assemble  waits until every sender's flag reached the epoch, runs
+ *                      the CSR chain over [local rows | received rows]
+ *                      (txb_scatter_add's np.add.at order), acks the epoch.
+ * `windows` is a DEVICE array of `world` window pointers valid in this process
+ * (own window + opened peers); `slot_bytes` a device array of each window's
+ * slot size.  Spins time out after TXB_HALO_TIMEOUT_MS (default 10 s) and
+ * record an error instead of hanging (txb_halo_window_error). */
+int64_t txb_halo_window_bytes(int64_t n_recv_rows, int n_comp, int dtype_bytes);
+int txb_halo_window_alloc(int64_t bytes, void** window, void* ipc_handle);
+int txb_halo_window_open(const void* ipc_handle, void** window);
+int txb_halo_window_close(void* window);
+int txb_halo_window_free(void* window);
+int txb_halo_window_error(void* window, int* error);
+int txb_halo_put(int dtype_bytes, int n_comp, int rank, int world, int64_t n_send,
+                 const int64_t* send_rows, const int32_t* send_peer, const int64_t* send_dst,
+                 const void* elem, void* const* windows, const int64_t* slot_bytes,
+                 const int32_t* out_peers, int n_out_peers, uint64_t epoch, void* stream);
+int txb_halo_assemble(int dtype_bytes, int n_comp, int rank, int world, int64_t n_owned,
+                      const int64_t* offsets, const int32_t* incidence, int64_t n_local_rows,
+                      const void* elem, void* const* windows, int64_t my_slot_bytes,
+                      const int32_t* in_peers, int n_in_peers, uint64_t epoch, void* out, void* stream);
 
 /* Debug timeline of txb_integrate_cells launches made by THIS thread: each
  * later launch takes the next 4*grid u64 of `device_buf` (capacity in u64) and

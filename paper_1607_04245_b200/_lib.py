@@ -40,6 +40,15 @@ SIGNATURES = {
     "txb_compute_geometry": (_I, [_I, c_int64, _P, _P, _P, _P, POINTER(c_int64), _P]),
     "txb_stream_probe": (_I, [_P, c_int64, _P, c_int64, _P]),
     "txb_debug_trace": (_I, [_P, c_int64]),
+    "txb_halo_window_bytes": (c_int64, [c_int64, _I, _I]),
+    "txb_halo_window_alloc": (_I, [c_int64, POINTER(c_void_p), _P]),
+    "txb_halo_window_open": (_I, [_P, POINTER(c_void_p)]),
+    "txb_halo_window_close": (_I, [_P]),
+    "txb_halo_window_free": (_I, [_P]),
+    "txb_halo_window_error": (_I, [_P, POINTER(c_int)]),
+    "txb_halo_put": (_I, [_I, _I, _I, _I, c_int64, _P, _P, _P, _P, _P, _P, _P, _I, ctypes.c_uint64, _P]),
+    "txb_halo_assemble": (_I, [_I, _I, _I, _I, c_int64, _P, _P, c_int64, _P, _P, c_int64, _P, _I,
+                               ctypes.c_uint64, _P, _P]),
     "txb_jit_compile": (_I, [c_char_p, c_char_p, c_char_p, _I, _I, _I, _I, _I, _I, _I, POINTER(c_void_p)]),
     "txb_jit_source": (c_char_p, [_P]),
     "txb_jit_log": (c_char_p, [_P]),

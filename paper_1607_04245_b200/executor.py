@@ -276,7 +276,8 @@ def integrate_mesh(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: Quadr
 
 def integrate_partitioned(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: QuadratureRule,
                           form: PhysicsForm, coeffs_global, aux: Optional[CellAux] = None, *, rank: int,
-                          world: int, exchange=None, dtype="f64", plan=None, align: int = 256, n_bl: int = 0):
+                          world: int, exchange=None, dtype="f64", plan=None, align: int = 256, n_bl: int = 0,
+                          peer=None):
     """One rank's share of integrate_transposed for the contiguous cell-range
     partition over ``world`` ranks (shard.cell_range): integrate the rank's
     cells on its GPU, then the halo exchange + assembly of halo.py.
@@ -285,19 +286,24 @@ def integrate_partitioned(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule
     (n_owned * n_comp,)), plan).  Concatenating every rank's owned entries
     reproduces the reference residual (executor.py:266, np.add.at order) bit
     for bit.  ``exchange``: halo.all_to_all_exchange() under torch.distributed
-    (None for world == 1).  ``plan``: a cached halo.build_halo_plan result."""
+    (None for world == 1).  ``plan``: a cached halo.build_halo_plan result.
+    ``peer``: a halo.PeerHalo — the exchange over peer memory (txb_halo_put /
+    txb_halo_assemble) instead of ``exchange``; its plan is used."""
     from . import halo
 
     torch = _torch()
     dt = scalar_dtype(dtype)
     form.require_aux(aux)
+    if peer is not None:
+        plan = peer.plan
     if plan is None:
         plan = halo.build_halo_plan(mesh.cells, mesh.n_vertices, rank, world, align)
     lo, hi = plan.lo, plan.hi
     n_b, nc = tab.n_b, form.n_comp
     sub = Mesh(mesh.dim, mesh.vertices, np.ascontiguousarray(mesh.cells[lo:hi]))
     tdt = torch.float32 if dt == np.float32 else torch.float64
-    buf = torch.empty((plan.n_local_rows + plan.n_recv, nc), dtype=tdt, device="cuda")
+    recv_rows = 0 if peer is not None else plan.n_recv  # the peer path receives into its window
+    buf = torch.empty((plan.n_local_rows + recv_rows, nc), dtype=tdt, device="cuda")
     elem = buf[:plan.n_local_rows].view(hi - lo, n_b, nc)
     if hi > lo:
         kernel = _resolve_backend(None, form, rule.n_q, aux, dt.itemsize)
@@ -312,5 +318,8 @@ def integrate_partitioned(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule
             blocks = gather_coefficients(sub, layout, glob_dev, cells=cells_dev)
             integrate_cells(tab, rule, CellGeometry(_dev(g.inv_jacobians, torch, dt), _dev(g.determinants, torch, dt)),
                             blocks, aux_dev, form, dtype=dt, out=elem, n_bl=n_bl)
-    owned = halo.assemble_owned(plan, buf, nc, exchange)
+    if peer is not None:
+        owned = peer.exchange_assemble(buf)
+    else:
+        owned = halo.assemble_owned(plan, buf, nc, exchange)
     return plan.owned, owned.reshape(-1), plan

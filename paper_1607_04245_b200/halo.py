@@ -24,6 +24,12 @@ Data path per rank (all on the device, nothing allocated by the library):
 The plan (ownership, send lists, CSR) is computed once per mesh and
 partition on the host from the connectivity; every rank derives the same
 plan independently, so no metadata is exchanged.
+
+Peer-memory variant (``PeerHalo``, csrc/txb_halo.cu): steps 2-4 without NCCL
+— ``txb_halo_put`` stores the owed rows straight into the owner's window (a
+device buffer shared by CUDA IPC handle; P2P stores over NVLink) and raises
+an epoch flag there; ``txb_halo_assemble`` waits on the flags and runs the same
+CSR chain over [local rows | window rows].  Same plan, same bits.
 """
 
 from __future__ import annotations
@@ -35,7 +41,8 @@ import numpy as np
 
 from .shard import all_ranges
 
-__all__ = ["HaloPlan", "build_halo_plan", "assemble_owned", "all_to_all_exchange"]
+__all__ = ["HaloPlan", "build_halo_plan", "assemble_owned", "all_to_all_exchange", "PeerHalo",
+           "local_peer_group", "distributed_peer_halo", "peer_send_layout"]
 
 
 @dataclass
@@ -182,3 +189,179 @@ def assemble_owned(plan: HaloPlan, buf, n_comp: int, exchange: Optional[Callable
                                      dev["incidence"].data_ptr(), buf.data_ptr(), out.data_ptr(), stream),
                    "halo assemble")
     return out[:plan.owned.size]
+
+
+# ---------------------------------------------------------------------------
+# Peer-memory exchange (txb_halo_put / txb_halo_assemble): the same plan, the
+# same chain, without NCCL — each rank stores its owed rows straight into the
+# owner's window (P2P over NVLink within a node) and the owner's assembly
+# kernel waits on per-sender epoch flags.
+# ---------------------------------------------------------------------------
+
+def slot_bytes(n_recv: int, n_comp: int, dtype_bytes: int) -> int:
+    """Bytes of one receive slot (txb_halo_window_bytes = 2048 + 2 slots)."""
+    return (max(n_recv, 1) * n_comp * dtype_bytes + 255) // 256 * 256
+
+
+def peer_send_layout(plan: HaloPlan, recv_counts_of: list):
+    """Where this rank's owed rows land: for each send row, the destination
+    rank and its row in that rank's receive slot.  ``recv_counts_of[p]`` is
+    rank p's plan.recv_counts; rank p's slot holds the rows of senders
+    s = p+1.. in ascending order, each sender's rows in (vertex, cell) order —
+    the order p's CSR expects (build_halo_plan)."""
+    r = plan.rank
+    peers, dsts = [], []
+    o = 0
+    for p in range(plan.world):
+        c = plan.send_counts[p]
+        if not c:
+            continue
+        base = int(sum(recv_counts_of[p][:r]))
+        if recv_counts_of[p][r] != c:
+            raise ValueError(f"rank {r} owes {c} rows to rank {p}, which expects {recv_counts_of[p][r]}")
+        peers.append(np.full(c, p, dtype=np.int32))
+        dsts.append(base + np.arange(c, dtype=np.int64))
+        o += c
+    send_peer = np.concatenate(peers) if peers else np.zeros(0, dtype=np.int32)
+    send_dst = np.concatenate(dsts) if dsts else np.zeros(0, dtype=np.int64)
+    out_peers = np.array([p for p in range(plan.world) if plan.send_counts[p]], dtype=np.int32)
+    in_peers = np.array([s for s in range(plan.world) if plan.recv_counts[s]], dtype=np.int32)
+    return send_peer, send_dst, out_peers, in_peers
+
+
+class PeerHalo:
+    """One rank's peer-memory halo exchange.  Build with ``local_peer_group``
+    (all ranks in this process: tests, single-GPU emulation) or
+    ``distributed_peer_halo`` (one process per GPU, windows shared by CUDA
+    IPC handle).  ``exchange_assemble(rows)`` is one residual evaluation."""
+
+    def __init__(self, plan: HaloPlan, n_comp: int, dtype_bytes: int, windows: list, recv_counts_of: list,
+                 on_close=None):
+        import torch
+
+        self.plan, self.n_comp, self.dtype_bytes = plan, n_comp, dtype_bytes
+        self.epoch = 0
+        self.window = windows[plan.rank]
+        self._on_close = on_close
+        send_peer, send_dst, out_peers, in_peers = peer_send_layout(plan, recv_counts_of)
+        dev = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt) if len(a) else  # noqa: E731
+                                             np.zeros(1, dtype=dt)).cuda()
+        self._d = {
+            "send_rows": dev(plan.send_rows, np.int64), "send_peer": dev(send_peer, np.int32),
+            "send_dst": dev(send_dst, np.int64), "out_peers": dev(out_peers, np.int32),
+            "in_peers": dev(in_peers, np.int32),
+            "windows": dev(np.array(windows, dtype=np.uint64).view(np.int64), np.int64),  # device void*[world]
+            "slot_bytes": dev(np.array([slot_bytes(sum(rc), n_comp, dtype_bytes) for rc in recv_counts_of],
+                                       dtype=np.int64), np.int64),
+        }
+        self.n_out, self.n_in = int(out_peers.size), int(in_peers.size)
+        self.my_slot = slot_bytes(plan.n_recv, n_comp, dtype_bytes)
+
+    def exchange_assemble(self, rows):
+        """rows: CUDA tensor (n_local_rows, n_comp) — this rank's element rows.
+        Returns the owned-vertex residual (n_owned, n_comp).  Asynchronous."""
+        import ctypes
+
+        import torch
+
+        from . import _lib
+
+        plan, nc, s = self.plan, self.n_comp, self.dtype_bytes
+        if tuple(rows.shape) != (plan.n_local_rows, nc) or rows.element_size() != s or not rows.is_contiguous():
+            raise ValueError(f"rows must be a contiguous ({plan.n_local_rows}, {nc}) tensor of {s}-byte scalars")
+        self.epoch += 1
+        d = self._d
+        dc = plan.device_arrays(torch)
+        L = _lib.lib()
+        stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        ptr = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        _lib.check(L.txb_halo_put(s, nc, plan.rank, plan.world, plan.n_send, ptr(d["send_rows"]), ptr(d["send_peer"]),
+                                  ptr(d["send_dst"]), ptr(rows), ptr(d["windows"]), ptr(d["slot_bytes"]),
+                                  ptr(d["out_peers"]), self.n_out, self.epoch, stream), "txb_halo_put")
+        out = torch.empty((max(plan.owned.size, 1), nc), dtype=rows.dtype, device=rows.device)
+        _lib.check(L.txb_halo_assemble(s, nc, plan.rank, plan.world, plan.owned.size, ptr(dc["offsets"]),
+                                       ptr(dc["incidence"]), plan.n_local_rows, ptr(rows), ptr(d["windows"]),
+                                       self.my_slot, ptr(d["in_peers"]), self.n_in, self.epoch, ptr(out), stream),
+                   "txb_halo_assemble")
+        return out[:plan.owned.size]
+
+    def check(self) -> None:
+        """Raise if a put or an assembly timed out waiting for a peer (host sync)."""
+        import ctypes
+
+        from . import _lib
+        from .errors import CudaLaneError
+
+        e = ctypes.c_int(0)
+        _lib.check(_lib.lib().txb_halo_window_error(ctypes.c_void_p(self.window), ctypes.byref(e)))
+        if e.value:
+            raise CudaLaneError(f"halo exchange on rank {self.plan.rank} timed out waiting for a peer "
+                                f"({'ack' if e.value == 1 else 'rows'}; TXB_HALO_TIMEOUT_MS)")
+
+    def close(self) -> None:
+        if self._on_close is not None:
+            self._on_close()
+            self._on_close = None
+
+
+def _alloc_window(n_recv: int, n_comp: int, dtype_bytes: int, ipc: bool):
+    import ctypes
+
+    from . import _lib
+
+    L = _lib.lib()
+    w = ctypes.c_void_p()
+    handle = ctypes.create_string_buffer(64) if ipc else None
+    _lib.check(L.txb_halo_window_alloc(L.txb_halo_window_bytes(n_recv, n_comp, dtype_bytes), ctypes.byref(w),
+                                       handle), "txb_halo_window_alloc")
+    return w.value, (handle.raw if ipc else None)
+
+
+def local_peer_group(plans: list, n_comp: int, dtype_bytes: int) -> list:
+    """PeerHalo objects for ALL ranks in this process (one device): tests and
+    single-GPU emulation.  Launch every rank's exchange in rank-independent
+    order on one stream: puts only wait for acks of two epochs back."""
+    from . import _lib
+
+    windows = [_alloc_window(p.n_recv, n_comp, dtype_bytes, False)[0] for p in plans]
+    recv_counts_of = [p.recv_counts for p in plans]
+
+    def free():
+        for w in windows:
+            _lib.lib().txb_halo_window_free(w)
+
+    group = [PeerHalo(p, n_comp, dtype_bytes, windows, recv_counts_of) for p in plans]
+    group[0]._on_close = free
+    return group
+
+
+def distributed_peer_halo(plan: HaloPlan, n_comp: int, dtype_bytes: int, group=None) -> PeerHalo:
+    """One process per GPU of one node: allocate this rank's window, share it by
+    CUDA IPC handle (torch.distributed all_gather_object, once), open the
+    peers' windows (P2P over NVLink)."""
+    import ctypes
+
+    import torch.distributed as dist
+
+    from . import _lib
+
+    own, handle = _alloc_window(plan.n_recv, n_comp, dtype_bytes, True)
+    infos = [None] * plan.world
+    dist.all_gather_object(infos, (handle, list(plan.recv_counts)), group=group)
+    L = _lib.lib()
+    windows, opened = [], []
+    for r, (h, _) in enumerate(infos):
+        if r == plan.rank:
+            windows.append(own)
+            continue
+        w = ctypes.c_void_p()
+        _lib.check(L.txb_halo_window_open(ctypes.create_string_buffer(h, 64), ctypes.byref(w)), "txb_halo_window_open")
+        windows.append(w.value)
+        opened.append(w.value)
+
+    def close():
+        for w in opened:
+            L.txb_halo_window_close(w)
+        L.txb_halo_window_free(own)
+
+    return PeerHalo(plan, n_comp, dtype_bytes, windows, [rc for _, rc in infos], on_close=close)

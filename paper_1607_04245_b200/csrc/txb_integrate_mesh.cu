@@ -87,6 +87,13 @@ __device__ __forceinline__ void mesh_slice(const MeshArgs<T>& a, const int64_t* 
       const int cell = c0 + lc;
       int64_t ids[NB];
       load_row<int64_t, NB, SMEM>(s_cells + cell * NB, ids);
+      // gather (mesh.py:202-217): coefficient block of the cell's vertices --
+      // issued before the geometry so its L2 latency overlaps the coordinates'
+      T cf[NBC];
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int c = 0; c < NCOMP; ++c) cf[b * NCOMP + c] = __ldg(a.coeffs_global + ids[b] * NCOMP + c);
       T J[DD];
       T det;
       if constexpr (GEOM == 0) {
@@ -106,12 +113,6 @@ __device__ __forceinline__ void mesh_slice(const MeshArgs<T>& a, const int64_t* 
         load_row<T, DD, SMEM>(s_inv + cell * DD, J);
         det = s_det[cell];
       }
-      // gather (mesh.py:202-217): coefficient block of the cell's vertices
-      T cf[NBC];
-#pragma unroll
-      for (int b = 0; b < NB; ++b)
-#pragma unroll
-        for (int c = 0; c < NCOMP; ++c) cf[b * NCOMP + c] = __ldg(a.coeffs_global + ids[b] * NCOMP + c);
 
       // standard P1 pull-back (see the exactness note in txb_kernels.cuh)
       T tr[NB][D];

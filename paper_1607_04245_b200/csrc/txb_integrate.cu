@@ -344,7 +344,8 @@ static bool pick_kernel(const Config& c, bool std_tab, KernelInfo& k) {
 }
 
 template <typename T>
-static int launch_t(const Config& c, const KernelInfo& k, const Geometry& g, int64_t n_cells, const void* basis,
+static int launch_t(bool zero_copy, const Config& c, const KernelInfo& k, const Geometry& g, int64_t n_cells,
+                    const void* basis,
                     const void* basis_der, const void* weights, const void* inv_j, const void* det_j,
                     const void* coeffs, const void* aux, void* out, cudaStream_t stream) {
   IntegrateArgs<T> a;
@@ -378,10 +379,13 @@ static int launch_t(const Config& c, const KernelInfo& k, const Geometry& g, int
   auto al16 = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
   const int nb = c.dim + 1, auxw = c.aux == 1 ? 1 : (c.aux == 2 ? nb : 0);
   auto sized16 = [&](int per_cell) { return ((int64_t)g.n_bc * per_cell * (int64_t)sizeof(T)) % 16 == 0; };
-  a.bulk = al16(inv_j) && al16(det_j) && al16(coeffs) && (c.aux == 0 || al16(aux)) && sized16(c.dim * c.dim) &&
-           sized16(1) && sized16(nb * c.n_comp) && (c.aux == 0 || sized16(auxw)) &&
+  // (zero_copy: the arrays are mapped pinned HOST memory; the bulk copies read
+  // them over PCIe -- measured as fast as staged copies, while per-lane loads
+  // from host memory were 1.3x slower -- and the L2 prefetch is skipped)
+  a.bulk = al16(inv_j) && al16(det_j) && al16(coeffs) && (c.aux == 0 || al16(aux)) &&
+           sized16(c.dim * c.dim) && sized16(1) && sized16(nb * c.n_comp) && (c.aux == 0 || sized16(auxw)) &&
            env_int("TXB_DISABLE_BULK", 0) == 0;
-  a.prefetch = prefetch_batches(g);
+  a.prefetch = zero_copy ? 0 : prefetch_batches(g);
   a.trace = next_trace_slot(g.grid);
   fill_tab(a.tab, c.n_q, c.dim + 1, c.dim, basis, basis_der, weights);
   void* params[] = {&a};
@@ -401,7 +405,7 @@ static int launch_t(const Config& c, const KernelInfo& k, const Geometry& g, int
 
 int integrate_device(const Config& c, int n_b, int64_t n_cells, const void* basis, const void* basis_der,
                      const void* weights, const void* inv_j, const void* det_j, const void* coeffs,
-                     const void* aux, void* out, int n_bl, int n_cb, cudaStream_t stream) {
+                     const void* aux, void* out, int n_bl, int n_cb, cudaStream_t stream, bool zero_copy = false) {
   int rc = validate(c);
   if (rc) return rc;
   if (n_b != c.dim + 1) {
@@ -430,8 +434,10 @@ int integrate_device(const Config& c, int n_b, int64_t n_cells, const void* basi
     return TXB_E_ARG;
   }
   if (c.dtype == 4)
-    return launch_t<float>(c, k, g, n_cells, basis, basis_der, weights, inv_j, det_j, coeffs, aux, out, stream);
-  return launch_t<double>(c, k, g, n_cells, basis, basis_der, weights, inv_j, det_j, coeffs, aux, out, stream);
+    return launch_t<float>(zero_copy, c, k, g, n_cells, basis, basis_der, weights, inv_j, det_j, coeffs, aux, out,
+                           stream);
+  return launch_t<double>(zero_copy, c, k, g, n_cells, basis, basis_der, weights, inv_j, det_j, coeffs, aux, out,
+                          stream);
 }
 
 // ---------------------------------------------------------------------------
@@ -489,6 +495,43 @@ int integrate_host(const Config& c, int n_b, int64_t n_cells, const void* basis,
   const int auxw = c.aux == 1 ? 1 : (c.aux == 2 ? nb : 0);
   const int64_t per_cell[5] = {(int64_t)c.dim * c.dim * s, s, (int64_t)nb * c.n_comp * s,
                                (int64_t)auxw * s, (int64_t)nb * c.n_comp * s};
+
+  // Zero copy: when every buffer is pinned host memory mapped into the device
+  // address space (cudaHostAlloc / torch pin_memory under UVA), the kernel's
+  // bulk copies read the inputs and its stores write the element vectors over
+  // PCIe directly: one launch, no device staging buffers, the H2D and D2H
+  // streams overlapping each other and the arithmetic.  Same PCIe-bound speed
+  // as the staged path (profiles/r1s_e2e.md).  Pageable buffers take the
+  // staged, pipelined path below.
+  if (env_int("TXB_HOST_ZERO_COPY", 1)) {
+    const void* hp[5] = {inv_j, det_j, coeffs, aux, out};
+    void* dp[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    bool mapped = true;
+    for (int r = 0; r < 5 && mapped; ++r) {
+      if (r == 3 && !auxw) continue;
+      cudaPointerAttributes at;
+      if (cudaPointerGetAttributes(&at, hp[r]) != cudaSuccess || at.type != cudaMemoryTypeHost ||
+          !at.devicePointer) {
+        cudaGetLastError();
+        mapped = false;
+        break;
+      }
+      dp[r] = at.devicePointer;
+    }
+    if (mapped) {
+      int dev = 0;
+      TXB_CUDA_TRY(cudaGetDevice(&dev));
+      std::lock_guard<std::mutex> lk(g_host_mu);
+      HostPathState* st = nullptr;
+      int rc0 = host_state(dev, 0, st);
+      if (rc0) return rc0;
+      rc0 = integrate_device(c, n_b, n_cells, basis, basis_der, weights, dp[0], dp[1], dp[2], auxw ? dp[3] : nullptr,
+                             dp[4], n_bl, n_cb, st->streams[0], true);
+      if (rc0) return rc0;
+      TXB_CUDA_TRY(cudaStreamSynchronize(st->streams[0]));
+      return TXB_OK;
+    }
+  }
   int64_t cell_bytes = 0;
   for (int64_t v : per_cell) cell_bytes += v;
   // Pieces of ~TXB_HOST_PIECE_MB MiB (multiple of 64 cells, keeps every slice 16B aligned).

@@ -233,3 +233,26 @@ def test_integrate_transposed_with_a_user_form():
                                   inv, det, co)
     want = oracle.scatter_add(mesh.cells, elem, mesh.n_vertices)
     assert bitwise_equal(res, want)
+
+
+# ---- codegen.generate_kernel_source (txfem/codegen.py:50-256) --------------------
+
+def test_generate_kernel_source_mirrors_reference_codegen():
+    from paper_1607_04245_b200.codegen import generate_kernel_source
+
+    geom = txb.derive_execution_geometry(3, 4, 1, 1, 8, 2, 1000)
+    f = txb.poisson_varcoef_form(3)
+    ks = generate_kernel_source(geom, f, "f64")
+    assert "f1_poisson_varcoef" in ks.text and ks.entry_name == "txb_jit_integrate"
+    assert ks.specialization == (3, 4, 1, 1, 8, "double")
+    assert generate_kernel_source(geom, f, "f64").text == ks.text  # deterministic
+    assert isinstance(ks.kernel, txb.JitKernel)
+    with pytest.raises(txb.CodegenError):
+        generate_kernel_source(geom, f, "f16")
+    with pytest.raises(txb.CodegenError):  # form / geometry mismatch
+        generate_kernel_source(txb.derive_execution_geometry(2, 3, 1, 1, 8, 2, 100), f, "f32")
+    with pytest.raises(txb.CodegenError):
+        generate_kernel_source(geom, txb.user_form("nosrc", 3, 1, None, 0, ""), "f32")
+    two = txb.derive_execution_geometry(3, 4, 1, 2, 4, 2, 1000)
+    ks2 = generate_kernel_source(two, form_of("advect", 3), "f32", aux_space="p1")
+    assert "#define TXB_HAS_F0 1" in ks2.text and "#define TXB_GRAD_A 1" in ks2.text

@@ -13,7 +13,7 @@
 //                   shared-memory stages with cp.async.bulk (SASS UBLKCP):
 //                   the batch's contiguous inv_j / det_j / coeffs / aux byte
 //                   ranges, completion counted on a `full` mbarrier
-//                   (expect_tx); it refills a stage once every consumer warp
+//                   (expect_tx); it refills a stage once every consumer lane
 //                   has arrived on the stage's `empty` mbarrier.
 //   consumer warps  each owns warp slices of CW = 32 / N_q cells of a batch:
 //     quadrature phase  lane <-> (cell, q): pulled-back gradients, grad u,

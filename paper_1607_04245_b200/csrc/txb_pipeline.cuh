@@ -110,7 +110,8 @@ __device__ __forceinline__ void load_row(const T* __restrict__ p, T (&r)[N]) {
 //                                              must be read from global memory
 // Consumer warps wait on the stage's `full` barrier and call
 //     consume(stage_ptr or nullptr, c0, ncell)
-// then arrive on `empty`.  A count of 0 published in the stage info stops them.
+// then every consumer lane arrives on `empty`.  A count of 0 published in the
+// stage info stops them.
 // ---------------------------------------------------------------------------
 struct PipelineSmem {
   uint64_t* full;

@@ -562,7 +562,8 @@ def main():
             "unit": "GF/s", "n_gpus": args.gpus, "steps": len(ts), "warmup": args.warmup,
             "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": dtype, "data": "synthetic (Kuhn mesh, seeded N(0,1) coefficients, P0 kappa)",
-            "config": {"workload": f"{args.config}: 3D P1 var-coef Laplacian, {r['n']} cells"},
+            "config": {"workload": f"{args.config}: {dim}D P1 {physics}, {r['n']} cells "
+                                   f"({per_gpu} per GPU x {max(world, args.gpus)})"},
             "cpu_baseline": {"value": gf, "unit": "GF/s", "cores": r["cores"], "kind": r["kind"],
                              "sample": f"{r['n']} cells per step, fork pool of {r['cores']} processes over "
                                        f"contiguous ranges, reference _kernels_cy lane"},

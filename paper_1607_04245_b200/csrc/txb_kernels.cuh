@@ -109,14 +109,25 @@ static int validate(const Config& c) {
 
 static int gcd(int a, int b) { return b ? gcd(b, a % b) : a; }
 
-// Default N_bl: batch near TXB_TARGET_CELLS (256) cells, N_bc a multiple of
-// the warp slice CW = 32/N_q so no warp slice is partial.
+// Cells per batch, measured on B200 at 2^20 cells (profiles/r1v_batch_sweep.md):
+// 128 everywhere except the 2D configurations whose N_bc steps are 96 cells
+// (N_b = 3 and CW = 32), where 192 wins for the scalar f32 and the f64
+// elasticity forms (10.0 vs 11.0 us, 23.4 vs 24.8 us).  The generic run-time
+// compiled kernel keeps 256 cells in f32 (15.6 us at 128 vs 14.7 us at 256).
+static int tuned_target_cells(const Config& c) {
+  if (c.form < 0) return c.dtype == 8 ? 128 : 256;  // run-time compiled kernels (more scratch per cell)
+  if (c.dim == 2 && c.n_q == 1 && ((c.n_comp == 1 && c.dtype == 4) || (c.n_comp == 2 && c.dtype == 8))) return 192;
+  return 128;
+}
+
+// Default N_bl: batch near the tuned target (TXB_TARGET_CELLS overrides), N_bc
+// a multiple of the warp slice CW = 32/N_q so no warp slice is partial.
 static void default_decomposition(const Config& c, int& n_bl, int& n_cb) {
   const int nbs = (c.dim + 1) * c.n_q;
   if (n_bl <= 0) {
     const int cw = 32 / c.n_q;
     const int step = cw / gcd(cw, nbs);  // n_bl multiple of step -> N_bc multiple of cw
-    const int target = env_int("TXB_TARGET_CELLS", c.dtype == 8 ? 128 : 256);
+    const int target = env_int("TXB_TARGET_CELLS", tuned_target_cells(c));
     int best = step, best_err = 1 << 30;
     for (int m = 1; m * step * nbs <= 1024; ++m) {
       const int err = std::abs(m * step * nbs - target);

@@ -120,6 +120,16 @@ static int tuned_target_cells(const Config& c) {
   return 128;
 }
 
+// Bytes of batch loads to keep in flight per SM (the ring-depth heuristic's
+// target), measured like the batch size (profiles/r1v_batch_sweep.md): 96 KB
+// except 3D var-coef f64 (the headline; 96 KB costs it an occupancy step,
+// 26.0 -> 31.4 us) and 2D var-coef f32, which stay at 72 KB.
+static int tuned_inflight_kb(const Config& c) {
+  if (c.form < 0) return 72;
+  if (c.n_comp == 1 && ((c.dim == 3 && c.dtype == 8) || (c.dim == 2 && c.dtype == 4))) return 72;
+  return 96;
+}
+
 // Default N_bl: batch near the tuned target (TXB_TARGET_CELLS overrides), N_bc
 // a multiple of the warp slice CW = 32/N_q so no warp slice is partial.
 static void default_decomposition(const Config& c, int& n_bl, int& n_cb) {
@@ -237,7 +247,7 @@ static int compute_geometry(const Config& c, const KernelInfo& k, int64_t n_cell
   // per SM.  Deeper rings only queue more requests and lengthen the launch
   // ramp (measured, profiles/r1_sweep.md).  TXB_STAGES forces a depth.
   const int forced = env_int("TXB_STAGES", 0);
-  const int64_t inflight_target = (int64_t)env_int("TXB_INFLIGHT_KB", 72) * 1024;
+  const int64_t inflight_target = (int64_t)env_int("TXB_INFLIGHT_KB", tuned_inflight_kb(c)) * 1024;
   auto occupancy = [&](int smem) {
     int occ = 1;
     if (query_device) {

@@ -300,6 +300,7 @@ static bool pick_mesh_form(const Config& c, KernelInfo& k) {
   {                                                                         \
     using K = MeshKernel<T, D, NQ, NCOMP, FORM, AUX, GEOM>;                 \
     k = {K::fn(), K::stage_bytes, K::scratch, K::CW};                       \
+    k.family = FAMILY_MESH;                                                 \
     return true;                                                            \
   }
   if (c.form == 0) TXB_MK(1, 0, 0)

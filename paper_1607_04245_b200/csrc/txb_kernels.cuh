@@ -109,35 +109,38 @@ static int validate(const Config& c) {
 
 static int gcd(int a, int b) { return b ? gcd(b, a % b) : a; }
 
-// Cells per batch, measured on B200 at 2^20 cells (profiles/r1v_batch_sweep.md):
-// 128 everywhere except the 2D configurations whose N_bc steps are 96 cells
-// (N_b = 3 and CW = 32), where 192 wins for the scalar f32 and the f64
-// elasticity forms (10.0 vs 11.0 us, 23.4 vs 24.8 us).  The generic run-time
-// compiled kernel keeps 256 cells in f32 (15.6 us at 128 vs 14.7 us at 256).
-static int tuned_target_cells(const Config& c) {
-  if (c.form < 0) return c.dtype == 8 ? 128 : 256;  // run-time compiled kernels (more scratch per cell)
+// Kernel families sharing the launch-geometry logic.
+enum KernelFamily { FAMILY_CELLS = 0, FAMILY_MESH = 1, FAMILY_JIT = 2 };
+
+// Cells per batch and in-flight bytes per SM (the ring-depth target),
+// measured on B200 (profiles/r1v_batch_sweep.md).  Launch-sized problems
+// (< 2^22 cells) favour smaller batches -- a shorter ramp and tail -- for the
+// cell-array kernels: 128 cells except the 2D configurations whose N_bc steps
+// are 96 cells, where 192 wins for scalar f32 and f64 elasticity; 96 KB in
+// flight except 3D var-coef f64 (96 KB costs it an occupancy step: 26.0 ->
+// 31.4 us) and 2D var-coef f32.  Streaming-sized problems keep the batches that
+// amortise the per-batch overhead best (f32 256 cells: 3D var-coef f32 at 2^24
+// 190 vs 208 us), as do the mesh-fused and run-time compiled kernels.
+static int tuned_target_cells(const Config& c, int family, int64_t n_cells) {
+  if (family != FAMILY_CELLS || n_cells >= ((int64_t)1 << 22)) return c.dtype == 8 ? 128 : 256;
   if (c.dim == 2 && c.n_q == 1 && ((c.n_comp == 1 && c.dtype == 4) || (c.n_comp == 2 && c.dtype == 8))) return 192;
   return 128;
 }
 
-// Bytes of batch loads to keep in flight per SM (the ring-depth heuristic's
-// target), measured like the batch size (profiles/r1v_batch_sweep.md): 96 KB
-// except 3D var-coef f64 (the headline; 96 KB costs it an occupancy step,
-// 26.0 -> 31.4 us) and 2D var-coef f32, which stay at 72 KB.
-static int tuned_inflight_kb(const Config& c) {
-  if (c.form < 0) return 72;
+static int tuned_inflight_kb(const Config& c, int family, int64_t n_cells) {
+  if (family != FAMILY_CELLS || n_cells >= ((int64_t)1 << 22)) return 72;
   if (c.n_comp == 1 && ((c.dim == 3 && c.dtype == 8) || (c.dim == 2 && c.dtype == 4))) return 72;
   return 96;
 }
 
 // Default N_bl: batch near the tuned target (TXB_TARGET_CELLS overrides), N_bc
 // a multiple of the warp slice CW = 32/N_q so no warp slice is partial.
-static void default_decomposition(const Config& c, int& n_bl, int& n_cb) {
+static void default_decomposition(const Config& c, int family, int64_t n_cells, int& n_bl, int& n_cb) {
   const int nbs = (c.dim + 1) * c.n_q;
   if (n_bl <= 0) {
     const int cw = 32 / c.n_q;
     const int step = cw / gcd(cw, nbs);  // n_bl multiple of step -> N_bc multiple of cw
-    const int target = env_int("TXB_TARGET_CELLS", tuned_target_cells(c));
+    const int target = env_int("TXB_TARGET_CELLS", tuned_target_cells(c, family, n_cells));
     int best = step, best_err = 1 << 30;
     for (int m = 1; m * step * nbs <= 1024; ++m) {
       const int err = std::abs(m * step * nbs - target);
@@ -161,6 +164,7 @@ struct KernelInfo {
   int rt_region[4];
   int rt_s;
   int rt_scratch;
+  int family;  // KernelFamily (0: the ahead-of-time cell-array kernels)
   int stage(int n_bc) const {
     if (stage_bytes) return stage_bytes(n_bc);
     int b = 0;
@@ -210,7 +214,7 @@ static DeviceProps device_props(int dev) {
 
 static int compute_geometry(const Config& c, const KernelInfo& k, int64_t n_cells, int n_bl, int n_cb,
                             bool query_device, Geometry& g) {
-  default_decomposition(c, n_bl, n_cb);
+  default_decomposition(c, k.family, n_cells, n_bl, n_cb);
   const int nb = c.dim + 1;
   const int64_t n_bc64 = (int64_t)n_bl * nb * c.n_q;
   const int64_t n_t64 = n_bc64 * c.n_comp;
@@ -247,7 +251,7 @@ static int compute_geometry(const Config& c, const KernelInfo& k, int64_t n_cell
   // per SM.  Deeper rings only queue more requests and lengthen the launch
   // ramp (measured, profiles/r1_sweep.md).  TXB_STAGES forces a depth.
   const int forced = env_int("TXB_STAGES", 0);
-  const int64_t inflight_target = (int64_t)env_int("TXB_INFLIGHT_KB", tuned_inflight_kb(c)) * 1024;
+  const int64_t inflight_target = (int64_t)env_int("TXB_INFLIGHT_KB", tuned_inflight_kb(c, k.family, n_cells)) * 1024;
   auto occupancy = [&](int smem) {
     int occ = 1;
     if (query_device) {

@@ -52,7 +52,9 @@ namespace txb {
 // One warp slice: CW cells starting at batch-local cell `c0` of a batch with
 // `ncell` cells whose per-cell arrays start at the given pointers (shared
 // stage or global memory); element vectors go to `out` (batch base, global).
-template <typename T, int D, int NQ, int NCOMP, int FORM, int AUX, bool STD, bool VEC>
+// FULLS: the slice is known to be full (CW cells) -- no bounds checks, no
+// divergent regions (the common case: full batches, one slice per warp).
+template <typename T, int D, int NQ, int NCOMP, int FORM, int AUX, bool STD, bool VEC, bool FULLS = false>
 __device__ __forceinline__ void warp_slice(const Tabulation<T>& tab, const T* __restrict__ s_inv,
                                            const T* __restrict__ s_det, const T* __restrict__ s_coef,
                                            const T* __restrict__ s_aux, unsigned char* __restrict__ scratch,
@@ -62,13 +64,13 @@ __device__ __forceinline__ void warp_slice(const Tabulation<T>& tab, const T* __
   constexpr int AUXW = AUX == 1 ? 1 : (AUX == 2 ? NB : 0);
   T* s_tr = reinterpret_cast<T*>(scratch);
   T* s_f1 = reinterpret_cast<T*>(scratch + S::TR_BYTES);
-  const int nc = min(S::CW, ncell - c0);
+  const int nc = FULLS ? S::CW : min(S::CW, ncell - c0);
 
   // ---------------- quadrature phase: lane <-> (cell, q) ----------------
   {
     const int lc = NQ == 1 ? lane : lane / NQ;
     const int q = NQ == 1 ? 0 : lane - lc * NQ;
-    if (lc < nc) {
+    if (lc < nc) {  // with FULLS, nc == CW: folds away when N_q divides 32
       const int cell = c0 + lc;
       T J[DD];
       load_row<T, DD, VEC>(s_inv + cell * DD, J);
@@ -191,7 +193,7 @@ __device__ __forceinline__ void warp_slice(const Tabulation<T>& tab, const T* __
     o_base[o] = e;
   };
   constexpr int FULL = S::CW * NBC;
-  if (nc == S::CW && FULL % 32 == 0) {
+  if (FULL % 32 == 0 && (FULLS || nc == S::CW)) {
 #pragma unroll
     for (int s = 0; s < FULL / 32; ++s) entry(s * 32 + lane);
   } else {
@@ -270,9 +272,15 @@ integrate_kernel(const __grid_constant__ IntegrateArgs<T> a) {
       const T* s_det = reinterpret_cast<const T*>(st + L::inv_bytes(nbc));
       const T* s_coef = reinterpret_cast<const T*>(st + L::inv_bytes(nbc) + L::det_bytes(nbc));
       const T* s_aux = reinterpret_cast<const T*>(st + L::inv_bytes(nbc) + L::det_bytes(nbc) + L::coef_bytes(nbc));
-      for (int c = warp * S::CW; c < ncell; c += W * S::CW)
-        warp_slice<T, D, NQ, NCOMP, FORM, AUX, STD, true>(a.tab, s_inv, s_det, s_coef, s_aux, scratch, c, ncell,
-                                                         out, lane);
+      // full batch, one slice per warp: the check-free slice (scalar forms; for
+      // elasticity the second instantiation costs registers and a stack frame)
+      if (NCOMP == 1 && ncell == nbc && nbc == W * S::CW)
+        warp_slice<T, D, NQ, NCOMP, FORM, AUX, STD, true, NCOMP == 1>(a.tab, s_inv, s_det, s_coef, s_aux,
+                                                                     scratch, warp * S::CW, ncell, out, lane);
+      else
+        for (int c = warp * S::CW; c < ncell; c += W * S::CW)
+          warp_slice<T, D, NQ, NCOMP, FORM, AUX, STD, true>(a.tab, s_inv, s_det, s_coef, s_aux, scratch, c, ncell,
+                                                           out, lane);
     } else {
       // unaligned caller buffers or an odd-sized partial batch: straight from global memory
       const T* g_aux = AUX != 0 ? a.aux + c0 * L::AUXW : nullptr;

@@ -228,28 +228,34 @@ def test_linearity_at_scale():
         assert bitwise_equal(e(x)[sl].cpu().numpy(), ref)
 
 
-def test_max_size_fp32_3d_2_27_cells():
-    """Maximum size of BASELINE configs[4] (2^27 cells) on one GPU: constant
-    coefficients on replicated Kuhn geometry -> exactly zero everywhere, and
-    a replicated random field reproduces the 2^20 golden output in every slab."""
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_max_size_3d_2_27_cells(dtype):
+    """Maximum size of BASELINE configs[4] (2^27 cells) on one GPU, both
+    precisions (f64: 20 GB of per-cell arrays): a replicated random field
+    reproduces the 2^20 golden output in every slab checked, and constant
+    coefficients on the replicated Kuhn geometry give exactly zero everywhere."""
     n_base = 1 << 20
     e = BIG["3d_varcoef_p0_1048576"]
     w = make_workload(3, "varcoef_p0", n_base, e["seed"])
-    inv, det, co, aux = w.cast("f32")
+    inv, det, co, aux = w.cast(dtype)
     reps = 128
     inv_b = inv.repeat(reps, 1, 1)
     det_b = det.repeat(reps)
     co_b = co.repeat(reps, 1, 1)
     aux_b = CellAux("p0", aux.values.repeat(reps, 1))
+    del inv, det
     out = torch.empty_like(co_b)
-    txb.integrate_cells(w.tab, w.rule, txb.CellGeometry(inv_b, det_b), co_b, aux_b, w.form, dtype="f32", out=out)
+    txb.integrate_cells(w.tab, w.rule, txb.CellGeometry(inv_b, det_b), co_b, aux_b, w.form, dtype=dtype, out=out)
     torch.cuda.synchronize()
+    want = e["cy_f32"] if dtype == "f32" else e["ref_f64"]
     for r in (0, 1, reps // 2, reps - 1):
-        assert _sha(out[r * n_base:(r + 1) * n_base]) == e["cy_f32"]
-    ones = torch.ones_like(co_b)
-    txb.integrate_cells(w.tab, w.rule, txb.CellGeometry(inv_b, det_b), ones, aux_b, w.form, dtype="f32", out=out)
+        assert _sha(out[r * n_base:(r + 1) * n_base]) == want
+    co_b.fill_(1.0)
+    txb.integrate_cells(w.tab, w.rule, txb.CellGeometry(inv_b, det_b), co_b, aux_b, w.form, dtype=dtype, out=out)
     torch.cuda.synchronize()
     assert int((out != 0).sum()) == 0
+    del inv_b, det_b, co_b, aux_b, out
+    torch.cuda.empty_cache()
 
 
 def test_back_to_back_launches_see_each_others_writes():

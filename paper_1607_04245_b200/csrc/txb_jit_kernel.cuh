@@ -33,11 +33,14 @@ constexpr int DD = D * D, NBC = NB * NCOMP;
 constexpr int AUXW = AUXM == 1 ? NAUX : (AUXM == 2 ? NB * NAUX : 0);
 constexpr int CW = 32 / NQ;  // cells per warp slice
 constexpr int S = (int)sizeof(real);
-// warp-private exchange area: T[q][b][k], f1s[q][c][k], f0s[q][c] per cell (odd strides)
-constexpr int TRS = make_odd(NQ * NB * D);
-constexpr int F1S = make_odd(NQ * NCOMP * D);
-constexpr int F0S = HAS_F0 ? make_odd(NQ * NCOMP) : 0;
-constexpr int SCRATCH_BYTES = round_up(CW * (TRS + F1S + F0S) * S, 16);
+// warp-private exchange area, component-major: row r of T (r = (q*NB+b)*D+k),
+// of f1s (r = (q*NCOMP+c)*D+k) and of f0s (r = q*NCOMP+c) holds the CW cells of
+// the slice at pitch P = CW + 4.  The quadrature-phase stores (lane = cell) hit
+// consecutive words; the basis-phase loads (lanes = (cell, b, c)) spread over
+// the banks (the cell-major odd stride left 4-way conflicts on the T loads).
+constexpr int P = CW + 4;
+constexpr int NTR = NQ * NB * D, NF1 = NQ * NCOMP * D, NF0 = HAS_F0 ? NQ * NCOMP : 0;
+constexpr int SCRATCH_BYTES = round_up(P * (NTR + NF1 + NF0) * S, 16);
 
 __device__ __forceinline__ int inv_bytes(int n) { return round_up(n * DD * S, 16); }
 __device__ __forceinline__ int det_bytes(int n) { return round_up(n * S, 16); }
@@ -50,8 +53,8 @@ __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const re
                                            const real* __restrict__ s_aux, real* __restrict__ scratch, int c0,
                                            int ncell, real* __restrict__ out, int lane) {
   real* s_tr = scratch;
-  real* s_f1 = s_tr + CW * TRS;
-  real* s_f0 = s_f1 + CW * F1S;
+  real* s_f1 = s_tr + P * NTR;
+  real* s_f0 = s_f1 + P * NF1;
   const int nc = min(CW, ncell - c0);
 
   // ---------------- quadrature phase: lane <-> (cell, q) ----------------
@@ -75,7 +78,7 @@ __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const re
 #pragma unroll
         for (int j = 0; j < D; ++j) acc = add(acc, mul(tab.D[(q * NB + b) * D + j], J[j * D + k]));
         tr[b][k] = acc;
-        s_tr[lc * TRS + (q * NB + b) * D + k] = acc;
+        s_tr[((q * NB + b) * D + k) * P + lc] = acc;
       }
 
     // u and grad u at the point (_kernels_py.py:44-51)
@@ -128,10 +131,10 @@ __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const re
     for (int c = 0; c < NCOMP; ++c) {
       const realv f1 = TXB_F1(u, gradU, a, gradA, c);
 #pragma unroll
-      for (int k = 0; k < D; ++k) s_f1[lc * F1S + (q * NCOMP + c) * D + k] = mul(mul(f1[k], det), w);
+      for (int k = 0; k < D; ++k) s_f1[((q * NCOMP + c) * D + k) * P + lc] = mul(mul(f1[k], det), w);
 #if TXB_HAS_F0
       const real f0 = TXB_F0(u, gradU, a, gradA, c);
-      s_f0[lc * F0S + q * NCOMP + c] = mul(mul(f0, det), w);
+      s_f0[(q * NCOMP + c) * P + lc] = mul(mul(f0, det), w);
 #endif
     }
   }
@@ -148,10 +151,10 @@ __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const re
     real e = real(0);  // _kernels_py.py:67-75: q-major, f0 term then the k terms
 #pragma unroll
     for (int qq = 0; qq < NQ; ++qq) {
-      if constexpr (HAS_F0) e = add(e, mul(tab.B[qq * NB + b], s_f0[ec * F0S + qq * NCOMP + c]));
+      if constexpr (HAS_F0) e = add(e, mul(tab.B[qq * NB + b], s_f0[(qq * NCOMP + c) * P + ec]));
 #pragma unroll
       for (int k = 0; k < D; ++k)
-        e = add(e, mul(s_tr[ec * TRS + (qq * NB + b) * D + k], s_f1[ec * F1S + (qq * NCOMP + c) * D + k]));
+        e = add(e, mul(s_tr[((qq * NB + b) * D + k) * P + ec], s_f1[((qq * NCOMP + c) * D + k) * P + ec]));
     }
     o_base[o] = e;
   };

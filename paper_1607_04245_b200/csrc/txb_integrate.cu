@@ -95,7 +95,7 @@ __device__ __forceinline__ void warp_slice(const Tabulation<T>& tab, const T* __
           for (int k = 0; k < D; ++k) tr[bb][k] = J[(bb - 1) * D + k];
         if (q == 0) {
 #pragma unroll
-          for (int k = 0; k < D; ++k) s_tr[lc * S::TRS + k] = tr[0][k];
+          for (int k = 0; k < D; ++k) s_tr[S::tr(lc, k)] = tr[0][k];
         }
       } else {
         const T* Dq = tab.D + q * NB * D;
@@ -107,7 +107,7 @@ __device__ __forceinline__ void warp_slice(const Tabulation<T>& tab, const T* __
 #pragma unroll
             for (int j = 1; j < D; ++j) acc = add(acc, mul(Dq[bb * D + j], J[j * D + k]));
             tr[bb][k] = acc;
-            s_tr[lc * S::TRS + (q * NB + bb) * D + k] = acc;
+            s_tr[S::tr(lc, (q * NB + bb) * D + k)] = acc;
           }
       }
 
@@ -136,7 +136,7 @@ __device__ __forceinline__ void warp_slice(const Tabulation<T>& tab, const T* __
       (void)a0;
 
       const T wq = tab.W[q];
-      T* f1_out = s_f1 + lc * S::F1S + q * NCOMP * D;
+
 #pragma unroll
       for (int c = 0; c < NCOMP; ++c)
 #pragma unroll
@@ -149,7 +149,7 @@ __device__ __forceinline__ void warp_slice(const Tabulation<T>& tab, const T* __
           } else {
             fv = mul(T(0.5), add(g[c][k], g[k][c]));
           }
-          f1_out[c * D + k] = mul(mul(fv, det), wq);
+          s_f1[S::f1(lc, (q * NCOMP + c) * D + k)] = mul(mul(fv, det), wq);
         }
     }
   }
@@ -163,32 +163,29 @@ __device__ __forceinline__ void warp_slice(const Tabulation<T>& tab, const T* __
     const int r = o - lc * NBC;
     const int b = r / NCOMP;
     const int c = r - b * NCOMP;
-    // f1s rows of this entry's component: one vector load when N_comp == 1
+    // f1s rows of this entry's component
     T f1[NQ * D];
-    if constexpr (NCOMP == 1 && S::F1S == NQ * D) {
-      load_row<T, NQ * D>(s_f1 + lc * S::F1S, f1);
-    } else {
 #pragma unroll
-      for (int q = 0; q < NQ; ++q)
+    for (int q = 0; q < NQ; ++q)
 #pragma unroll
-        for (int k = 0; k < D; ++k) f1[q * D + k] = s_f1[lc * S::F1S + (q * NCOMP + c) * D + k];
-    }
+      for (int k = 0; k < D; ++k) f1[q * D + k] = s_f1[S::f1(lc, (q * NCOMP + c) * D + k)];
     T e = T(0);  // the output chain starts at +0 exactly as the reference's
     if constexpr (STD) {
-      const T* tp = b == 0 ? s_tr + lc * S::TRS : s_inv + (c0 + lc) * DD + (b - 1) * D;
+      // T[0] from the exchange area, T[b>=1] = invJ row b-1 of the stage
+      const T* tp = b == 0 ? s_tr + S::tr(lc, 0) : s_inv + (c0 + lc) * DD + (b - 1) * D;
+      const int step = b == 0 ? S::tr(0, 1) - S::tr(0, 0) : 1;
       T t[D];
 #pragma unroll
-      for (int k = 0; k < D; ++k) t[k] = tp[k];
+      for (int k = 0; k < D; ++k) t[k] = tp[k * step];
 #pragma unroll
       for (int q = 0; q < NQ; ++q)
 #pragma unroll
         for (int k = 0; k < D; ++k) e = add(e, mul(t[k], f1[q * D + k]));
     } else {
-      const T* tp = s_tr + lc * S::TRS + b * D;
 #pragma unroll
       for (int q = 0; q < NQ; ++q)
 #pragma unroll
-        for (int k = 0; k < D; ++k) e = add(e, mul(tp[q * NB * D + k], f1[q * D + k]));
+        for (int k = 0; k < D; ++k) e = add(e, mul(s_tr[S::tr(lc, (q * NB + b) * D + k)], f1[q * D + k]));
     }
     o_base[o] = e;
   };

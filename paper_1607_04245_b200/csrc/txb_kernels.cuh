@@ -37,22 +37,28 @@ struct StageLayout {
   }
 };
 
-// Warp-private exchange area between the two phases.  STD (standard P1
-// tables): only T[0][k] is stored (the other rows are invJ rows, read from the
-// stage); otherwise all T[q][b][k].  T strides are odd (bank-conflict free
-// scalar access); the f1 rows are padded to 16 bytes so the basis phase reads
-// them with vector loads (a warp touches 32/(N_b N_comp) cells per access).
+// Warp-private exchange area between the two phases: T (STD: only T[0][k] --
+// the other rows are invJ rows, read from the stage; otherwise all
+// T[q][b][k]) and f1s.  Scalar forms use a component-major layout: row r (T:
+// r = k or (q*N_b+b)*D+k; f1s: r = (q*N_comp+c)*D+k) holds the slice's CW
+// cells at pitch P = CW + 4, so the quadrature-phase stores (lane = cell) hit
+// consecutive words and the basis-phase loads (lanes = (cell, b)) spread over
+// the banks (3D var-coef f64 25.85 -> 25.23 us).  Vector forms keep a
+// cell-major layout with odd strides, which measured faster for them.
 template <typename T, int D, int NQ, int NCOMP, bool STD>
 struct Scratch {
   static constexpr int NB = D + 1;
   static constexpr int CW = 32 / NQ;  // cells per warp slice
+  static constexpr bool CM = NCOMP == 1;
+  static constexpr int P = CW + 4;
   static constexpr int TR = STD ? D : NQ * NB * D;
   static constexpr int F1 = NQ * NCOMP * D;
-  static constexpr int VEC = 16 / (int)sizeof(T);
   static constexpr int TRS = make_odd(TR);
-  static constexpr int F1S = NCOMP == 1 ? round_up(F1, VEC) : make_odd(F1);
-  static constexpr int TR_BYTES = round_up(CW * TRS * (int)sizeof(T), 16);
-  static constexpr int BYTES = TR_BYTES + CW * F1S * (int)sizeof(T);
+  static constexpr int F1S = make_odd(F1);
+  __device__ static int tr(int lc, int r) { return CM ? r * P + lc : lc * TRS + r; }
+  __device__ static int f1(int lc, int r) { return CM ? r * P + lc : lc * F1S + r; }
+  static constexpr int TR_BYTES = round_up((CM ? P * TR : CW * TRS) * (int)sizeof(T), 16);
+  static constexpr int BYTES = TR_BYTES + round_up((CM ? P * F1 : CW * F1S) * (int)sizeof(T), 16);
 };
 
 // Exactness note (why the chains below may skip the reference's "acc = 0;

@@ -55,16 +55,22 @@ struct MeshStage {
   __host__ __device__ static int stage_bytes(int n) { return cell_bytes(n) + aux_bytes(n) + inv_bytes(n) + det_bytes(n); }
 };
 
-// Warp-private exchange: per cell the (cast) invJ rows = T[b>=1], T[0], and f1s.
+// Warp-private exchange: per cell the (cast) invJ rows = T[b>=1], T[0], and
+// f1s; component-major (pitch CW + 4) for the scalar forms, cell-major with
+// odd strides for elasticity (as the cell-array kernel's Scratch).
 template <typename T, int D, int NQ, int NCOMP>
 struct MeshScratch {
   static constexpr int CW = 32 / NQ;
-  static constexpr int TRS = make_odd(D * D + D);  // invJ (D*D) then T[0] (D)
+  static constexpr bool CM = NCOMP == 1;
+  static constexpr int P = CW + 4;
+  static constexpr int TR = D * D + D;  // invJ (D*D) then T[0] (D)
+  static constexpr int TRS = make_odd(TR);
   static constexpr int F1 = NQ * NCOMP * D;
-  static constexpr int VEC = 16 / (int)sizeof(T);
-  static constexpr int F1S = NCOMP == 1 ? round_up(F1, VEC) : make_odd(F1);
-  static constexpr int TR_BYTES = round_up(CW * TRS * (int)sizeof(T), 16);
-  static constexpr int BYTES = TR_BYTES + CW * F1S * (int)sizeof(T);
+  static constexpr int F1S = make_odd(F1);
+  __device__ static int tr(int lc, int r) { return CM ? r * P + lc : lc * TRS + r; }
+  __device__ static int f1(int lc, int r) { return CM ? r * P + lc : lc * F1S + r; }
+  static constexpr int TR_BYTES = round_up((CM ? P * TR : CW * TRS) * (int)sizeof(T), 16);
+  static constexpr int BYTES = TR_BYTES + round_up((CM ? P * F1 : CW * F1S) * (int)sizeof(T), 16);
 };
 
 template <typename T, int D, int NQ, int NCOMP, int FORM, int AUX, int GEOM, bool SMEM>
@@ -129,9 +135,9 @@ __device__ __forceinline__ void mesh_slice(const MeshArgs<T>& a, const int64_t* 
         for (int k = 0; k < D; ++k) tr[bb][k] = J[(bb - 1) * D + k];
       if (q == 0) {
 #pragma unroll
-        for (int i = 0; i < DD; ++i) s_tr[lc * S::TRS + i] = J[i];
+        for (int i = 0; i < DD; ++i) s_tr[S::tr(lc, i)] = J[i];
 #pragma unroll
-        for (int k = 0; k < D; ++k) s_tr[lc * S::TRS + DD + k] = tr[0][k];
+        for (int k = 0; k < D; ++k) s_tr[S::tr(lc, DD + k)] = tr[0][k];
       }
 
       T g[NCOMP][D];
@@ -159,7 +165,7 @@ __device__ __forceinline__ void mesh_slice(const MeshArgs<T>& a, const int64_t* 
       (void)a0;
 
       const T wq = a.tab.W[q];
-      T* f1_out = s_f1 + lc * S::F1S + q * NCOMP * D;
+
 #pragma unroll
       for (int c = 0; c < NCOMP; ++c)
 #pragma unroll
@@ -172,7 +178,7 @@ __device__ __forceinline__ void mesh_slice(const MeshArgs<T>& a, const int64_t* 
           } else {
             fv = mul(T(0.5), add(g[c][k], g[k][c]));
           }
-          f1_out[c * D + k] = mul(mul(fv, det), wq);
+          s_f1[S::f1(lc, (q * NCOMP + c) * D + k)] = mul(mul(fv, det), wq);
         }
     }
   }
@@ -187,20 +193,19 @@ __device__ __forceinline__ void mesh_slice(const MeshArgs<T>& a, const int64_t* 
     const int b = r / NCOMP;
     const int c = r - b * NCOMP;
     T f1[NQ * D];
-    if constexpr (NCOMP == 1 && S::F1S == NQ * D) {
-      load_row<T, NQ * D>(s_f1 + lc * S::F1S, f1);
-    } else {
 #pragma unroll
-      for (int q = 0; q < NQ; ++q)
+    for (int q = 0; q < NQ; ++q)
 #pragma unroll
-        for (int k = 0; k < D; ++k) f1[q * D + k] = s_f1[lc * S::F1S + (q * NCOMP + c) * D + k];
-    }
-    const T* tp = s_tr + lc * S::TRS + (b == 0 ? DD : (b - 1) * D);
+      for (int k = 0; k < D; ++k) f1[q * D + k] = s_f1[S::f1(lc, (q * NCOMP + c) * D + k)];
+    const int r0 = b == 0 ? DD : (b - 1) * D;  // T[0] after the invJ rows
+    T t[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) t[k] = s_tr[S::tr(lc, r0 + k)];
     T e = T(0);  // the output chain starts at +0 exactly as the reference's
 #pragma unroll
     for (int q = 0; q < NQ; ++q)
 #pragma unroll
-      for (int k = 0; k < D; ++k) e = add(e, mul(tp[k], f1[q * D + k]));
+      for (int k = 0; k < D; ++k) e = add(e, mul(t[k], f1[q * D + k]));
     o_base[o] = e;
   };
   constexpr int FULL = S::CW * NBC;

@@ -94,8 +94,15 @@ __device__ __forceinline__ void warp_slice(const Tabulation<T>& tab, const T* __
 #pragma unroll
           for (int k = 0; k < D; ++k) tr[bb][k] = J[(bb - 1) * D + k];
         if (q == 0) {
+          if constexpr (S::SJ) {
 #pragma unroll
-          for (int k = 0; k < D; ++k) s_tr[S::tr(lc, k)] = tr[0][k];
+            for (int i = 0; i < DD; ++i) s_tr[S::tr(lc, i)] = J[i];
+#pragma unroll
+            for (int k = 0; k < D; ++k) s_tr[S::tr(lc, DD + k)] = tr[0][k];
+          } else {
+#pragma unroll
+            for (int k = 0; k < D; ++k) s_tr[S::tr(lc, k)] = tr[0][k];
+          }
         }
       } else {
         const T* Dq = tab.D + q * NB * D;
@@ -171,12 +178,17 @@ __device__ __forceinline__ void warp_slice(const Tabulation<T>& tab, const T* __
       for (int k = 0; k < D; ++k) f1[q * D + k] = s_f1[S::f1(lc, (q * NCOMP + c) * D + k)];
     T e = T(0);  // the output chain starts at +0 exactly as the reference's
     if constexpr (STD) {
-      // T[0] from the exchange area, T[b>=1] = invJ row b-1 of the stage
-      const T* tp = b == 0 ? s_tr + S::tr(lc, 0) : s_inv + (c0 + lc) * DD + (b - 1) * D;
-      const int step = b == 0 ? S::tr(0, 1) - S::tr(0, 0) : 1;
       T t[D];
+      if constexpr (S::SJ) {  // all rows from the exchange area
+        const int r0 = b == 0 ? DD : (b - 1) * D;
 #pragma unroll
-      for (int k = 0; k < D; ++k) t[k] = tp[k * step];
+        for (int k = 0; k < D; ++k) t[k] = s_tr[S::tr(lc, r0 + k)];
+      } else {  // T[0] from the exchange area, T[b>=1] = invJ row b-1 of the stage
+        const T* tp = b == 0 ? s_tr + S::tr(lc, 0) : s_inv + (c0 + lc) * DD + (b - 1) * D;
+        const int step = b == 0 ? S::tr(0, 1) - S::tr(0, 0) : 1;
+#pragma unroll
+        for (int k = 0; k < D; ++k) t[k] = tp[k * step];
+      }
 #pragma unroll
       for (int q = 0; q < NQ; ++q)
 #pragma unroll

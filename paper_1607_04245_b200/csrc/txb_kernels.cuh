@@ -37,21 +37,26 @@ struct StageLayout {
   }
 };
 
-// Warp-private exchange area between the two phases: T (STD: only T[0][k] --
-// the other rows are invJ rows, read from the stage; otherwise all
-// T[q][b][k]) and f1s.  Scalar forms use a component-major layout: row r (T:
-// r = k or (q*N_b+b)*D+k; f1s: r = (q*N_comp+c)*D+k) holds the slice's CW
-// cells at pitch P = CW + 4, so the quadrature-phase stores (lane = cell) hit
-// consecutive words and the basis-phase loads (lanes = (cell, b)) spread over
-// the banks (3D var-coef f64 25.85 -> 25.23 us).  Vector forms keep a
-// cell-major layout with odd strides, which measured faster for them.
+// Warp-private exchange area between the two phases: T and f1s.  Scalar forms
+// use a component-major layout: row r holds the slice's CW cells at pitch
+// P = CW + 4 (T: with the standard tables T[0] at r = k -- or, for SJ, the
+// invJ rows = T[b>=1] at r = 0..D*D-1 and T[0] at r = D*D + k -- otherwise
+// T[q][b][k] at r = (q*N_b+b)*D+k; f1s: r = (q*N_comp+c)*D+k), so the
+// quadrature-phase stores (lane = cell) hit consecutive words and the
+// basis-phase loads (lanes = (cell, b)) spread over the banks.  Vector forms keep a
+// cell-major layout with odd strides (T[0] only; invJ rows from the stage),
+// which measured faster for them.
 template <typename T, int D, int NQ, int NCOMP, bool STD>
 struct Scratch {
   static constexpr int NB = D + 1;
   static constexpr int CW = 32 / NQ;  // cells per warp slice
   static constexpr bool CM = NCOMP == 1;
   static constexpr int P = CW + 4;
-  static constexpr int TR = STD ? D : NQ * NB * D;
+  // STD: SJ keeps the invJ rows (T[b>=1]) and T[0] in the exchange area
+  // (measured faster for 2D f32 only: 9.74 -> 9.15 us; 3D f32 and 2D f64 lose
+  // to the larger area), otherwise T[0] only, the invJ rows read from the stage
+  static constexpr bool SJ = CM && STD && D == 2 && sizeof(T) == 4;
+  static constexpr int TR = STD ? (SJ ? D * D + D : D) : NQ * NB * D;
   static constexpr int F1 = NQ * NCOMP * D;
   static constexpr int TRS = make_odd(TR);
   static constexpr int F1S = make_odd(F1);

@@ -543,6 +543,7 @@ def main():
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=3.0)
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (profiling runs)")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.warmup < 3:
@@ -615,9 +616,12 @@ def main():
     e2e_steps = max(3, min(20, args.steps // 20))
     if barrier:
         barrier()
-    e2e_s, h2d, d2h, _ = time_e2e(wl, e2e_steps, 2)
-    e2e_s = reduce_max(e2e_s)
-    e2e_gf = flops_cell * cells_total * e2e_steps / e2e_s / 1e9
+    if args.no_e2e:
+        e2e_s, h2d, d2h, e2e_gf = float("nan"), 0, 0, None
+    else:
+        e2e_s, h2d, d2h, _ = time_e2e(wl, e2e_steps, 2)
+        e2e_s = reduce_max(e2e_s)
+        e2e_gf = flops_cell * cells_total * e2e_steps / e2e_s / 1e9
 
     if rank != 0:
         if world > 1:

@@ -92,7 +92,7 @@ def main():
     md = [f"# ncu summary `{tag}` (B200, `--clock-control none`)", ""]
     lpath = OUT / f"{tag}_launches.csv"
     if lpath.exists():
-        md += ["## Launch list of `python bench.py --steps 20 --warmup 3 --no-variants --no-cpu`",
+        md += ["## Launch list of `python bench.py --steps 20 --warmup 3 --no-variants --no-cpu --no-e2e`",
                "(cold-cache, serialised per-launch times: compare shares, not absolutes; the stream probe",
                "and torch fills are bench.py's measurement scaffolding, outside the timed region)", "",
                launch_shares(lpath), ""]

@@ -278,3 +278,39 @@ def test_back_to_back_launches_see_each_others_writes():
         ref = -oracle.integrate(1, 1, B, D, W, inv, det, ref, aux)
     torch.cuda.synchronize()
     assert bitwise_equal(cur.cpu().numpy(), ref)
+
+
+# ---- property test: random problems over the whole configuration space -------
+from hypothesis import HealthCheck, given, settings, strategies as st  # noqa: E402
+
+
+@settings(max_examples=120, deadline=None, suppress_health_check=list(HealthCheck))
+@given(dim=st.integers(2, 3), form=st.sampled_from([(0, 0), (1, 1), (1, 2), (2, 0)]), n_q=st.integers(1, 8),
+       n=st.integers(0, 3000), dtype=st.sampled_from(["f64", "f32"]), tables=st.sampled_from(["p1", "random"]),
+       n_bl=st.sampled_from([0, 1, 3, 8, 17]), n_cb=st.sampled_from([0, 1, 5]), offset=st.sampled_from([0, 0, 1]),
+       seed=st.integers(0, 2 ** 16))
+def test_random_problems_bitwise(dim, form, n_q, n, dtype, tables, n_bl, n_cb, offset, seed):
+    """Any form, aux space, rule size, tabulation (standard P1 or random),
+    decomposition, size, alignment and precision: bit-identical to the oracle."""
+    fc, am = form
+    rng = np.random.default_rng(seed)
+    nb, nc = dim + 1, dim if fc == 2 else 1
+    if n_bl and n_bl * nb * n_q * nc > 1024:
+        n_bl = 1
+    if tables == "p1":
+        B1, D1, W1 = oracle.p1_tables(dim)
+        B, D, W = np.tile(B1, (n_q, 1)), np.tile(D1, (n_q, 1, 1)), np.full(n_q, W1[0] / n_q)
+    else:
+        B, D, W = rng.uniform(0, 1, (n_q, nb)), rng.uniform(-1, 1, (n_q, nb, dim)), rng.uniform(0.1, 0.5, n_q)
+    jac = np.eye(dim) + 0.3 * rng.uniform(-1, 1, (n, dim, dim))
+    inv = np.linalg.inv(jac) if n else np.zeros((0, dim, dim))
+    det = np.linalg.det(jac) if n else np.zeros(0)
+    co = rng.standard_normal((n, nb, nc))
+    aux = None
+    if am == 1:
+        aux = rng.uniform(0.5, 1.5, (n, 1))
+    elif am == 2:
+        aux = rng.uniform(0.5, 1.5, (n, nb, 1))
+    out = _run_device(fc, am, B, D, W, inv, det, co, aux, dtype, n_bl=n_bl, n_cb=n_cb, offset=offset)
+    ref = oracle.integrate(fc, am, B, D, W, inv, det, co, aux, DT[dtype][0])
+    assert bitwise_equal(out, ref)

@@ -256,3 +256,29 @@ def test_generate_kernel_source_mirrors_reference_codegen():
     two = txb.derive_execution_geometry(3, 4, 1, 2, 4, 2, 1000)
     ks2 = generate_kernel_source(two, form_of("advect", 3), "f32", aux_space="p1")
     assert "#define TXB_HAS_F0 1" in ks2.text and "#define TXB_GRAD_A 1" in ks2.text
+
+
+from hypothesis import HealthCheck, given, settings, strategies as st  # noqa: E402
+
+
+@pytest.mark.gpu
+@settings(max_examples=40, deadline=None, suppress_health_check=list(HealthCheck))
+@given(name=st.sampled_from(SPECS), dim=st.integers(2, 3), n_q=st.integers(1, 3), n=st.integers(0, 2500),
+       dtype=st.sampled_from([np.float64, np.float32]), n_bl=st.sampled_from([0, 1, 5]), seed=st.integers(0, 999))
+def test_jit_random_problems_bitwise(name, dim, n_q, n, dtype, n_bl, seed):
+    rng = np.random.default_rng(seed)
+    s = user_forms.spec(name, dim)
+    f = form_of(name, dim)
+    B = rng.uniform(0, 1, (n_q, dim + 1))
+    D = rng.uniform(-1, 1, (n_q, dim + 1, dim))
+    W = rng.uniform(0.1, 0.5, n_q)
+    jac = np.eye(dim) + 0.3 * rng.uniform(-1, 1, (n, dim, dim))
+    inv = np.linalg.inv(jac) if n else np.zeros((0, dim, dim))
+    det = np.linalg.det(jac) if n else np.zeros(0)
+    co = rng.standard_normal((n, dim + 1, s["n_comp"]))
+    aux = aux_for(s, n, rng)
+    k = txb.cuda_kernel(f, n_q, aux, np.dtype(dtype).itemsize)
+    got = _run(k, B, D, W, inv, det, co, aux, dtype, n_bl=n_bl)
+    want = oracle.integrate_forms(s["f1_many"], s["f0_many"], s["uses_grad_a"], s["aux"], B, D, W, inv, det, co,
+                                  None if aux is None else aux.values, dtype)
+    assert bitwise_equal(got, want)

@@ -304,6 +304,51 @@ ADVECT_F1 = f"realv f1_advect{_ADVECT_SIG}\n{{\n  return a[0]*gradU[comp] + u[co
 ADVECT_F0 = f"real f0_advect{_ADVECT_SIG}\n{{\n  return a[1]*u[comp] + dot(gradA[0], gradU[comp]);\n}}\n"
 
 
+def api_rows(steps=20):
+    """The reference's mesh-level call from the host (executor.integrate_transposed,
+    executor.py:161-267): numpy global coefficients in, numpy residual out, every
+    step (H2D of the coefficient vector, fused geometry-or-given + gather +
+    integration kernel, deterministic scatter-add, D2H of the residual).  Wall
+    time per call; the mesh's static device data is cached across calls."""
+    import torch
+
+    import paper_1607_04245_b200 as txb
+    from paper_1607_04245_b200.workload import PHYSICS, refine_for
+
+    rows = []
+    for name in ("3d_varcoef_f64", "3d_elasticity_f64"):
+        dim, physics, dtype, n = CONFIGS[name]
+        factory, aux_space = PHYSICS[physics]
+        form = factory(dim)
+        mesh = txb.generate_unit_simplex_mesh(dim, refine_for(dim, n))
+        layout = txb.FieldLayout(form.n_comp)
+        rule = txb.quadrature_rule(dim, 1)
+        tab = txb.tabulate(dim, rule)
+        glob = np.random.default_rng(3).standard_normal(layout.global_size(mesh))
+        aux = None
+        if aux_space == "p0":
+            aux = txb.CellAux("p0", np.random.default_rng(4).uniform(0.5, 1.5, (mesh.n_cells, 1)))
+        geom = txb.compute_geometry(mesh, device_out=True)  # mesh setup, once
+        n_bl = 128 // (dim + 1)  # 128-cell batches (the tuned batch size); n_cb only feeds the trace model
+        for label, cg in (("given_geometry", geom), ("geometry_in_kernel", None)):
+            for _ in range(3):
+                txb.integrate_transposed(mesh, layout, tab, rule, form, glob, aux, n_bl=n_bl, n_cb=8, dtype=dtype, shared_mem_limit=None,
+                                         cell_geom=cg)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                res, _ = txb.integrate_transposed(mesh, layout, tab, rule, form, glob, aux, n_bl=n_bl, n_cb=8,
+                                                  dtype=dtype, cell_geom=cg, shared_mem_limit=None)
+            dt = (time.perf_counter() - t0) / steps
+            rows.append({"config": f"api_integrate_transposed_{label}_{name}", "cells": mesh.n_cells,
+                         "vertices": mesh.n_vertices, "ms_per_call": dt * 1e3,
+                         "gcells_per_s": mesh.n_cells / dt / 1e9,
+                         "path": "host numpy in/out: H2D coefficients, fused mesh kernel, scatter-add, D2H residual"})
+        del geom
+        torch.cuda.empty_cache()
+    return rows
+
+
 def sweep_rows(peak):
     """BASELINE.json configs[4]: 3D P1 var-coef Laplacian at 2^24..2^27 cells on
     one GPU, f32 and f64.  The 2^20-cell Kuhn workload is tiled on the device
@@ -702,6 +747,7 @@ def main():
             torch.cuda.empty_cache()
         variants.extend(mesh_rows)
         variants.extend(sweep_rows(peak))
+        variants.extend(api_rows())
         variants.extend(jit_rows(peak, max(50, args.steps // 4)))
         line["variants"] = variants
     print(json.dumps(line), flush=True)

@@ -146,7 +146,12 @@ def execute_chunk(geom: ExecutionGeometry, tab: Tabulation, rule: QuadratureRule
     return elem, trace
 
 
+# Device copies of the last mesh's static data (connectivity, vertices, the
+# vertex incidence CSR), reused across residual evaluations of the same mesh
+# arrays (keyed on array identity, like the reference's Mesh, which is never
+# mutated in place).
 _INCIDENCE_CACHE: dict = {}
+_MESH_CACHE: dict = {}
 
 
 def _incidence_for(mesh: Mesh, cells_dev):
@@ -158,6 +163,19 @@ def _incidence_for(mesh: Mesh, cells_dev):
     _INCIDENCE_CACHE.clear()
     _INCIDENCE_CACHE[key] = (mesh.cells, inc)
     return inc
+
+
+def _mesh_on_device(mesh: Mesh, torch):
+    """(cells int64, vertices float64) CUDA tensors of ``mesh``, uploaded once."""
+    key = (id(mesh.cells), id(mesh.vertices), mesh.cells.shape, mesh.vertices.shape)
+    hit = _MESH_CACHE.get(key)
+    if hit is not None and hit[0] is mesh.cells and hit[1] is mesh.vertices:
+        return hit[2], hit[3]
+    cells = torch.from_numpy(np.ascontiguousarray(mesh.cells, dtype=np.int64)).to("cuda")
+    verts = torch.from_numpy(np.ascontiguousarray(mesh.vertices, dtype=np.float64)).to("cuda")
+    _MESH_CACHE.clear()
+    _MESH_CACHE[key] = (mesh.cells, mesh.vertices, cells, verts)
+    return cells, verts
 
 
 def integrate_transposed(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: QuadratureRule,
@@ -182,7 +200,7 @@ def integrate_transposed(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule:
         raise ShapeError(f"auxiliary data covers {aux.values.shape[0]} cells, expected {mesh.n_cells}")
     torch = _torch()
     host_out = isinstance(coeffs_global, np.ndarray) or not hasattr(coeffs_global, "is_cuda")
-    cells_dev = torch.from_numpy(np.ascontiguousarray(mesh.cells, dtype=np.int64)).to("cuda")
+    cells_dev, verts_dev = _mesh_on_device(mesh, torch)
     glob = coeffs_global if not host_out else np.asarray(coeffs_global, dtype=np.float64)
     glob_dev = _dev(glob, torch, dt)
     aux_dev = None if aux is None else CellAux(aux.space, _dev(aux.values, torch, dt))
@@ -190,7 +208,7 @@ def integrate_transposed(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule:
     if _mesh_fusable(tab, rule) and not isinstance(kernel, _backend.JitKernel):
         # geometry + gather + cast + integrate in one kernel (csrc/txb_integrate_mesh.cu)
         elem = integrate_mesh(mesh, layout, tab, rule, form, glob_dev, aux_dev, dtype=dt, cell_geom=cell_geom,
-                              cells=cells_dev, n_bl=n_bl)
+                              cells=cells_dev, vertices=verts_dev, n_bl=n_bl)
     else:
         if cell_geom is None:
             cell_geom = compute_geometry(mesh, cells=cells_dev, device_out=True)
@@ -200,10 +218,8 @@ def integrate_transposed(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule:
             blocks, aux_dev, form, dtype=dt, n_bl=n_bl, n_cb=n_cb)
     residual = scatter_add_element_vectors(mesh, layout, elem, incidence=_incidence_for(mesh, cells_dev))
 
-    trace = ExecutionTrace(geom=geom, scalar_width=dt.itemsize, remainder_cells=geom.n_r)
-    per_batch = model_batch_counters(geom, form, dt.itemsize, aux)
-    for ci in range(geom.n_chunks):
-        trace.chunks.append(ChunkTrace(chunk_index=ci, batches=[replace(per_batch) for _ in range(geom.n_cb)]))
+    trace = ExecutionTrace.uniform(geom, dt.itemsize, model_batch_counters(geom, form, dt.itemsize, aux),
+                                   remainder_cells=geom.n_r)
     if host_out:
         residual = residual.cpu().numpy()
     return residual, trace

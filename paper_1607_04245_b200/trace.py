@@ -10,7 +10,7 @@ reading ``trace.totals()`` or ``write_csv`` sees the reference's numbers.
 from __future__ import annotations
 
 import csv
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 from typing import IO, Optional
 
 from .physics import CellAux, PhysicsForm
@@ -55,16 +55,48 @@ class ChunkTrace:
         return sum(b.barriers for b in self.batches)
 
 
-@dataclass
 class ExecutionTrace:
-    geom: ExecutionGeometry
-    scalar_width: int
-    chunks: list = field(default_factory=list)
-    remainder_cells: int = 0
+    """Per-chunk counters of one integrate_transposed call (device.py:96-144).
+
+    The CUDA lane's counters are the closed-form model, identical for every
+    full batch, so a trace built with ``uniform`` stores one template and
+    materialises ``chunks`` (n_chunks x n_cb BatchCounters) only when read;
+    ``totals`` is closed-form.  (A 1 M-cell mesh has ~8,000 batches: building
+    them eagerly cost more host time than the GPU work of the call.)"""
+
+    def __init__(self, geom: ExecutionGeometry, scalar_width: int, chunks: Optional[list] = None,
+                 remainder_cells: int = 0):
+        self.geom = geom
+        self.scalar_width = scalar_width
+        self.remainder_cells = remainder_cells
+        self._chunks = list(chunks) if chunks is not None else []
+        self._uniform: Optional[BatchCounters] = None
+        self._n_chunks = 0
+
+    @classmethod
+    def uniform(cls, geom: ExecutionGeometry, scalar_width: int, per_batch: BatchCounters,
+                remainder_cells: int = 0) -> "ExecutionTrace":
+        t = cls(geom, scalar_width, remainder_cells=remainder_cells)
+        t._uniform, t._n_chunks = per_batch, geom.n_chunks
+        t._chunks = None
+        return t
+
+    @property
+    def chunks(self) -> list:
+        if self._chunks is None:
+            pb, n_cb = self._uniform, self.geom.n_cb
+            self._chunks = [ChunkTrace(chunk_index=ci, batches=[replace(pb) for _ in range(n_cb)])
+                            for ci in range(self._n_chunks)]
+        return self._chunks
 
     def totals(self) -> BatchCounters:
         agg = BatchCounters()
-        for chunk in self.chunks:
+        if self._chunks is None:  # closed form: every batch carries the template
+            n = self._n_chunks * self.geom.n_cb
+            for name in vars(agg):
+                setattr(agg, name, n * getattr(self._uniform, name))
+            return agg
+        for chunk in self._chunks:
             for b in chunk.batches:
                 for name in vars(agg):
                     setattr(agg, name, getattr(agg, name) + getattr(b, name))

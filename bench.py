@@ -304,6 +304,41 @@ ADVECT_F1 = f"realv f1_advect{_ADVECT_SIG}\n{{\n  return a[0]*gradU[comp] + u[co
 ADVECT_F0 = f"real f0_advect{_ADVECT_SIG}\n{{\n  return a[1]*u[comp] + dot(gradA[0], gradU[comp]);\n}}\n"
 
 
+def strong_scaling_rows(world, rank, barrier, reduce_max, steps=10):
+    """BASELINE.json configs[4] across the ranks: a FIXED total of 2^24 and 2^26
+    cells (f32 and f64) split into contiguous per-rank ranges (strong scaling;
+    the per-rank slice tiles the rank's 2^20-cell Kuhn workload, values do not
+    affect timing).  Device time of `steps` launches per rank, max over ranks."""
+    import torch
+
+    from paper_1607_04245_b200.physics import CellAux
+
+    rows = []
+    for dtype in ("f32", "f64"):
+        base = "3d_varcoef_" + dtype
+        vf, vb = config_model(base)
+        wl = rank_workload(base, rank, world)
+        for lg in (24, 26):
+            total = 1 << lg
+            n = total // world
+            reps = -(-n // wl["n"])
+            cut = lambda t: t.repeat(reps, *([1] * (t.dim() - 1)))[:n].contiguous()  # noqa: E731
+            big = dict(wl, n=n, inv=cut(wl["inv"]), det=cut(wl["det"]), coeffs=cut(wl["coeffs"]),
+                       aux=CellAux("p0", cut(wl["aux"].values)))
+            tot, _ = time_device(big, steps, 3, 1, barrier)
+            tot = reduce_max(tot)
+            ms = tot / steps
+            rows.append({"config": f"3d_varcoef_{dtype}_2^{lg}_total", "dtype": dtype, "cells_total": total,
+                         "cells_per_rank": n, "n_gpus": world, "ms_per_step": ms,
+                         "gflops": vf * total / (ms * 1e-3) / 1e9, "gbs": vb * total / (ms * 1e-3) / 1e9,
+                         "scaling": "strong"})
+            del big
+            torch.cuda.empty_cache()
+        del wl
+        torch.cuda.empty_cache()
+    return rows
+
+
 def api_rows(steps=20):
     """The reference's mesh-level call from the host (executor.integrate_transposed,
     executor.py:161-267): numpy global coefficients in, numpy residual out, every
@@ -668,6 +703,8 @@ def main():
         e2e_s = reduce_max(e2e_s)
         e2e_gf = flops_cell * cells_total * e2e_steps / e2e_s / 1e9
 
+    strong = strong_scaling_rows(world, rank, barrier, reduce_max) if world > 1 else None
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -750,6 +787,8 @@ def main():
         variants.extend(api_rows())
         variants.extend(jit_rows(peak, max(50, args.steps // 4)))
         line["variants"] = variants
+    if strong is not None:
+        line["strong_scaling"] = strong
     print(json.dumps(line), flush=True)
 
 

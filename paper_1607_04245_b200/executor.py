@@ -178,6 +178,23 @@ def _mesh_on_device(mesh: Mesh, torch):
     return cells, verts
 
 
+_PART_CACHE: dict = {}
+
+
+def _partition_on_device(mesh: Mesh, lo: int, hi: int, torch):
+    """(cells[lo:hi] int64, vertices float64) CUDA tensors of one rank's cell
+    range, uploaded once per (mesh arrays, range)."""
+    key = (id(mesh.cells), id(mesh.vertices), mesh.cells.shape, mesh.vertices.shape, lo, hi)
+    hit = _PART_CACHE.get(key)
+    if hit is not None and hit[0] is mesh.cells and hit[1] is mesh.vertices:
+        return hit[2], hit[3]
+    cells = torch.from_numpy(np.ascontiguousarray(mesh.cells[lo:hi], dtype=np.int64)).to("cuda")
+    verts = torch.from_numpy(np.ascontiguousarray(mesh.vertices, dtype=np.float64)).to("cuda")
+    _PART_CACHE.clear()
+    _PART_CACHE[key] = (mesh.cells, mesh.vertices, cells, verts)
+    return cells, verts
+
+
 def integrate_transposed(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: QuadratureRule,
                          form: PhysicsForm, coeffs_global, aux: Optional[CellAux] = None, *, n_bl: int,
                          n_cb: int, dtype: Union[str, np.dtype] = "f64", jobs: int = 1,
@@ -211,7 +228,7 @@ def integrate_transposed(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule:
                               cells=cells_dev, vertices=verts_dev, n_bl=n_bl)
     else:
         if cell_geom is None:
-            cell_geom = compute_geometry(mesh, cells=cells_dev, device_out=True)
+            cell_geom = compute_geometry(mesh, cells=cells_dev, vertices=verts_dev, device_out=True)
         blocks = gather_coefficients(mesh, layout, glob_dev, cells=cells_dev)
         elem = integrate_cells(
             tab, rule, CellGeometry(_dev(cell_geom.inv_jacobians, torch, dt), _dev(cell_geom.determinants, torch, dt)),
@@ -325,12 +342,12 @@ def integrate_partitioned(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule
         kernel = _resolve_backend(None, form, rule.n_q, aux, dt.itemsize)
         glob_dev = _dev(coeffs_global, torch, dt)
         aux_dev = None if aux is None else CellAux(aux.space, _dev(aux.values[lo:hi], torch, dt))
-        cells_dev = torch.from_numpy(sub.cells.astype(np.int64)).to("cuda")
+        cells_dev, verts_dev = _partition_on_device(mesh, lo, hi, torch)
         if _mesh_fusable(tab, rule) and not isinstance(kernel, _backend.JitKernel):
-            integrate_mesh(sub, layout, tab, rule, form, glob_dev, aux_dev, dtype=dt, cells=cells_dev, out=elem,
-                           n_bl=n_bl)
+            integrate_mesh(sub, layout, tab, rule, form, glob_dev, aux_dev, dtype=dt, cells=cells_dev,
+                           vertices=verts_dev, out=elem, n_bl=n_bl)
         else:
-            g = compute_geometry(sub, cells=cells_dev, device_out=True)
+            g = compute_geometry(sub, cells=cells_dev, vertices=verts_dev, device_out=True)
             blocks = gather_coefficients(sub, layout, glob_dev, cells=cells_dev)
             integrate_cells(tab, rule, CellGeometry(_dev(g.inv_jacobians, torch, dt), _dev(g.determinants, torch, dt)),
                             blocks, aux_dev, form, dtype=dt, out=elem, n_bl=n_bl)

@@ -143,13 +143,15 @@ def _to_device(x, torch, dtype=None):
     return t.contiguous(), False
 
 
-def compute_geometry(mesh: Mesh, *, cells=None, device_out: bool = False) -> CellGeometry:
+def compute_geometry(mesh: Mesh, *, cells=None, vertices=None, device_out: bool = False) -> CellGeometry:
     """Inverse Jacobians (J's k-th column = v_{k+1} - v_0) and detJ on the
     device, float64, cofactor formulas of mesh.py:150-190.  Raises
-    OrientationError naming the first cell with detJ <= 0."""
+    OrientationError naming the first cell with detJ <= 0.  ``cells`` /
+    ``vertices``: optional device copies (int64 / float64) of the mesh arrays."""
     torch = _torch()
     d = mesh.dim
-    X, _ = _to_device(np.ascontiguousarray(mesh.vertices, dtype=np.float64), torch)
+    X = vertices if vertices is not None else \
+        _to_device(np.ascontiguousarray(mesh.vertices, dtype=np.float64), torch)[0]
     C = cells if cells is not None else _to_device(np.ascontiguousarray(mesh.cells, dtype=np.int64), torch)[0]
     n = int(C.shape[0])
     inv = torch.empty((n, d, d), dtype=torch.float64, device="cuda")

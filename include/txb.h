@@ -17,6 +17,7 @@
  *                             + integrate_cells, fused into one kernel)
  *   txb_gather_coefficients   <- txfem/mesh.py:202-217 gather_coefficients
  *   txb_scatter_add           <- txfem/mesh.py:220-234 scatter_add_element_vectors
+ *   txb_scatter_add_slots     <- the same, vertices visited in element-row order
  *   txb_compute_geometry      <- txfem/mesh.py:150-190 compute_geometry
  *   txb_jit_compile / txb_jit_integrate
  *                          <- txfem/physics.py:260-304 user_form + the string-
@@ -154,6 +155,25 @@ int txb_gather_coefficients(int dtype_bytes, int64_t n_cells, int n_b, int n_com
 int txb_scatter_add(int dtype_bytes, int64_t n_vertices, int n_comp,
                     const int64_t* offsets, const int32_t* incidence,
                     const void* elem, void* out, void* stream);
+
+/* The same sums with the vertices visited in SLOT order (their first incident
+ * element row ascending, txb_build_scatter_order): slot t sums the list
+ * slot_incidence[slot_offsets[t] .. slot_offsets[t+1]) -- the list of vertex
+ * slot_vertex[t], unchanged -- into out[slot_vertex[t]].  Bit-identical to
+ * txb_scatter_add; neighbouring threads read neighbouring element rows even
+ * when the mesh numbers vertices and cells in different orders. */
+int txb_scatter_add_slots(int dtype_bytes, int64_t n_vertices, int n_comp,
+                          const int64_t* slot_offsets, const int32_t* slot_incidence,
+                          const int32_t* slot_vertex, const void* elem, void* out, void* stream);
+
+/* Slot order of a vertex CSR (offsets/incidence from txb_build_incidence,
+ * n_entries = offsets[n_vertices]): slot_vertex (n_vertices), slot_offsets
+ * (n_vertices+1), slot_incidence (n_entries).  `scratch` needs
+ * txb_scatter_order_scratch_bytes(n_vertices) bytes. */
+int64_t txb_scatter_order_scratch_bytes(int64_t n_vertices);
+int txb_build_scatter_order(int64_t n_vertices, int64_t n_entries, const int64_t* offsets,
+                            const int32_t* incidence, int64_t* slot_offsets, int32_t* slot_incidence,
+                            int32_t* slot_vertex, void* scratch, void* stream);
 
 /* Build the vertex incidence CSR on the device from the connectivity
  * (cells int64 (n, n_b)).  `offsets` has n_vertices+1 entries, `incidence`

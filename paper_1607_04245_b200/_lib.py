@@ -35,6 +35,9 @@ SIGNATURES = {
     "txb_integrate_mesh": (_I, [_I, _I, _I, _I, _I, _I, c_int64, c_int64] + [_P] * 11 + [_I, _P]),
     "txb_gather_coefficients": (_I, [_I, c_int64, _I, _I, _P, _P, _P, _P]),
     "txb_scatter_add": (_I, [_I, c_int64, _I, _P, _P, _P, _P, _P]),
+    "txb_scatter_add_slots": (_I, [_I, c_int64, _I, _P, _P, _P, _P, _P, _P]),
+    "txb_scatter_order_scratch_bytes": (c_int64, [c_int64]),
+    "txb_build_scatter_order": (_I, [c_int64, c_int64, _P, _P, _P, _P, _P, _P, _P]),
     "txb_incidence_scratch_bytes": (c_int64, [c_int64, _I, c_int64]),
     "txb_build_incidence": (_I, [c_int64, _I, c_int64, _P, _P, _P, _P, _P]),
     "txb_compute_geometry": (_I, [_I, c_int64, _P, _P, _P, _P, POINTER(c_int64), _P]),

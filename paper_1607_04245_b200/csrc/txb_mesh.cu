@@ -4,6 +4,8 @@
 //   txb_gather_coefficients  <- txfem/mesh.py:202-217  (E: global -> per-cell blocks)
 //   txb_build_incidence      vertex -> (cell, b) CSR in ascending cell order
 //   txb_scatter_add          <- txfem/mesh.py:220-234  (E^T: np.add.at order, no atomics)
+//   txb_build_scatter_order / txb_scatter_add_slots: the same sums visited in
+//                            element-row order (locality past the L2 size)
 //   txb_compute_geometry     <- txfem/mesh.py:150-190  (cofactor inverse, detJ > 0 check)
 //
 // Plus the library's error plumbing (txb_last_error).
@@ -58,12 +60,12 @@ constexpr int SCATTER_TPB = 256;
 template <typename T, int NCOMP>
 __global__ void __launch_bounds__(SCATTER_TPB)
 scatter_kernel(int64_t n_vertices, const int64_t* __restrict__ offsets, const int32_t* __restrict__ incidence,
-               const T* __restrict__ elem, T* __restrict__ out) {
+               const int32_t* __restrict__ slot_vertex, const T* __restrict__ elem, T* __restrict__ out) {
   constexpr int U = 8;
   const int64_t n = n_vertices * NCOMP;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < n; o += stride) {
-    const int64_t v = NCOMP == 1 ? o : o / NCOMP;
+    const int64_t v = NCOMP == 1 ? o : o / NCOMP;  // CSR row (vertex, or slot when slot_vertex)
     const int k = NCOMP == 1 ? 0 : (int)(o - v * NCOMP);
     int64_t e = offsets[v];
     const int64_t end = offsets[v + 1];
@@ -79,7 +81,55 @@ scatter_kernel(int64_t n_vertices, const int64_t* __restrict__ offsets, const in
       for (int u = 0; u < U; ++u)
         if (idx[u] >= 0) sum = add(sum, val[u]);
     }
-    out[o] = sum;
+    if (slot_vertex) out[(int64_t)__ldg(slot_vertex + v) * NCOMP + k] = sum;
+    else out[o] = sum;
+  }
+}
+
+// ---- scatter order.  The element rows are laid out in cell order, the
+// output in vertex order; when the two orders disagree (the reference's 3D
+// unit mesh numbers vertices x-fastest and cubes z-fastest,
+// txfem/mesh.py:113-127) the consecutive vertices of one warp read element
+// rows megabytes apart and, past the L2 size, every row costs a scattered DRAM
+// sector.  A SLOT order visits the vertices by their first incident element
+// row instead, so neighbouring threads read neighbouring rows; the CSR is
+// re-laid out in slot order (coalesced incidence reads) and slot_vertex[t]
+// says which vertex slot t writes.  Every vertex keeps its own chain, so the
+// sums are unchanged bit for bit.
+__global__ void first_row_keys_kernel(int64_t n_vertices, const int64_t* __restrict__ offsets,
+                                      const int32_t* __restrict__ incidence, int32_t sentinel, int32_t* keys,
+                                      int32_t* vals) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n_vertices; v += stride) {
+    const int64_t e = offsets[v];
+    keys[v] = e < offsets[v + 1] ? incidence[e] : sentinel;
+    vals[v] = (int32_t)v;
+  }
+}
+
+__global__ void slot_counts_kernel(int64_t n_slots, const int64_t* __restrict__ offsets,
+                                   const int32_t* __restrict__ slot_vertex, int64_t* counts) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_slots; t += stride) {
+    const int64_t v = slot_vertex[t];
+    counts[t] = offsets[v + 1] - offsets[v];
+  }
+}
+
+// One warp per 32 consecutive slots; the lanes copy each slot's list together
+// (coalesced stores into the slot-ordered CSR).
+__global__ void slot_copy_kernel(int64_t n_slots, const int64_t* __restrict__ offsets,
+                                 const int32_t* __restrict__ incidence, const int32_t* __restrict__ slot_vertex,
+                                 const int64_t* __restrict__ slot_offsets, int32_t* __restrict__ slot_incidence) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w * 32 < n_slots; w += warps) {
+    const int64_t t_end = w * 32 + 32 < n_slots ? w * 32 + 32 : n_slots;
+    for (int64_t t = w * 32; t < t_end; ++t) {
+      const int64_t v = slot_vertex[t];
+      const int64_t src = offsets[v], len = offsets[v + 1] - src, dst = slot_offsets[t];
+      for (int64_t i = lane; i < len; i += 32) slot_incidence[dst + i] = incidence[src + i];
+    }
   }
 }
 
@@ -152,8 +202,9 @@ extern "C" int txb_gather_coefficients(int dtype_bytes, int64_t n_cells, int n_b
   return TXB_OK;
 }
 
-extern "C" int txb_scatter_add(int dtype_bytes, int64_t n_vertices, int n_comp, const int64_t* offsets,
-                               const int32_t* incidence, const void* elem, void* out, void* stream) {
+static int scatter_impl(int dtype_bytes, int64_t n_vertices, int n_comp, const int64_t* offsets,
+                        const int32_t* incidence, const int32_t* slot_vertex, const void* elem, void* out,
+                        void* stream) {
   if (n_vertices < 0 || n_comp < 1 || n_comp > TXB_MAX_COMP) {
     set_error("scatter: bad sizes (n_vertices=%lld, n_comp=%d)", (long long)n_vertices, n_comp);
     return TXB_E_SHAPE;
@@ -170,7 +221,8 @@ extern "C" int txb_scatter_add(int dtype_bytes, int64_t n_vertices, int n_comp, 
   cudaStream_t s = (cudaStream_t)stream;
   const int blocks = (int)std::min<int64_t>((n_vertices * n_comp + SCATTER_TPB - 1) / SCATTER_TPB, 1 << 20);
 #define TXB_SCATTER(T, NC)                                                                                  \
-  scatter_kernel<T, NC><<<blocks, SCATTER_TPB, 0, s>>>(n_vertices, offsets, incidence, (const T*)elem, (T*)out)
+  scatter_kernel<T, NC><<<blocks, SCATTER_TPB, 0, s>>>(n_vertices, offsets, incidence, slot_vertex, (const T*)elem, \
+                                                        (T*)out)
   if (dtype_bytes == 8) {
     if (n_comp == 1) TXB_SCATTER(double, 1);
     else if (n_comp == 2) TXB_SCATTER(double, 2);
@@ -183,6 +235,22 @@ extern "C" int txb_scatter_add(int dtype_bytes, int64_t n_vertices, int n_comp, 
 #undef TXB_SCATTER
   TXB_CUDA_TRY(cudaGetLastError());
   return TXB_OK;
+}
+
+extern "C" int txb_scatter_add(int dtype_bytes, int64_t n_vertices, int n_comp, const int64_t* offsets,
+                               const int32_t* incidence, const void* elem, void* out, void* stream) {
+  return scatter_impl(dtype_bytes, n_vertices, n_comp, offsets, incidence, nullptr, elem, out, stream);
+}
+
+extern "C" int txb_scatter_add_slots(int dtype_bytes, int64_t n_vertices, int n_comp, const int64_t* slot_offsets,
+                                     const int32_t* slot_incidence, const int32_t* slot_vertex, const void* elem,
+                                     void* out, void* stream) {
+  if (n_vertices > 0 && !slot_vertex) {
+    set_error("scatter: NULL slot_vertex");
+    return TXB_E_ARG;
+  }
+  return scatter_impl(dtype_bytes, n_vertices, n_comp, slot_offsets, slot_incidence, slot_vertex, elem, out,
+                      stream);
 }
 
 // Scratch: keys_in, keys_out, vals_in (int32, n*n_b each), counts (int64,
@@ -244,6 +312,72 @@ extern "C" int txb_build_incidence(int64_t n_cells, int n_b, int64_t n_vertices,
                                                  (int64_t)n, 0, end_bit, s));
   }
   TXB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(temp, temp_b, counts, offsets, (int64_t)(n_vertices + 1), s));
+  return TXB_OK;
+}
+
+// Scratch: keys_in, keys_out, vals_in (int32, n_vertices each), counts
+// (int64, n_vertices+1), CUB temp storage for the radix sort and the scan.
+static size_t order_temp_bytes(int64_t n_vertices) {
+  size_t sort_b = 0, scan_b = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, sort_b, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                  (const int32_t*)nullptr, (int32_t*)nullptr, (int64_t)n_vertices);
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_b, (const int64_t*)nullptr, (int64_t*)nullptr,
+                                (int64_t)(n_vertices + 1));
+  return std::max(sort_b, scan_b);
+}
+
+extern "C" int64_t txb_scatter_order_scratch_bytes(int64_t n_vertices) {
+  if (n_vertices < 0) return 0;
+  return (int64_t)(3 * a256(n_vertices * sizeof(int32_t)) + a256((n_vertices + 1) * sizeof(int64_t)) +
+                   a256(order_temp_bytes(n_vertices)));
+}
+
+extern "C" int txb_build_scatter_order(int64_t n_vertices, int64_t n_entries, const int64_t* offsets,
+                                       const int32_t* incidence, int64_t* slot_offsets, int32_t* slot_incidence,
+                                       int32_t* slot_vertex, void* scratch, void* stream) {
+  if (n_vertices < 0 || n_entries < 0 || n_vertices >= ((int64_t)1 << 31) || n_entries >= ((int64_t)1 << 31)) {
+    set_error("scatter order: n_vertices and n_entries must be in [0, 2^31)");
+    return TXB_E_SHAPE;
+  }
+  if (!slot_offsets || (n_vertices > 0 && (!offsets || !slot_vertex || !scratch)) ||
+      (n_entries > 0 && (!incidence || !slot_incidence))) {
+    set_error("scatter order: NULL device pointer");
+    return TXB_E_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned char* p = (unsigned char*)scratch;
+  int32_t* keys_in = (int32_t*)p;
+  p += a256(n_vertices * sizeof(int32_t));
+  int32_t* keys_out = (int32_t*)p;
+  p += a256(n_vertices * sizeof(int32_t));
+  int32_t* vals_in = (int32_t*)p;
+  p += a256(n_vertices * sizeof(int32_t));
+  int64_t* counts = (int64_t*)p;
+  p += a256((n_vertices + 1) * sizeof(int64_t));
+  void* temp = p;
+  size_t temp_b = order_temp_bytes(n_vertices);
+
+  TXB_CUDA_TRY(cudaMemsetAsync(counts, 0, (n_vertices + 1) * sizeof(int64_t), s));
+  if (n_vertices > 0) {
+    // key = the vertex's first (smallest) element row; untouched vertices
+    // (empty lists, output +0) go last.  The radix sort is stable.
+    const int32_t sentinel = (int32_t)n_entries;
+    first_row_keys_kernel<<<blocks_for(n_vertices), TPB, 0, s>>>(n_vertices, offsets, incidence, sentinel,
+                                                                  keys_in, vals_in);
+    TXB_CUDA_TRY(cudaGetLastError());
+    int end_bit = 1;
+    while (end_bit < 31 && ((int64_t)1 << end_bit) <= n_entries) ++end_bit;
+    TXB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(temp, temp_b, keys_in, keys_out, vals_in, slot_vertex,
+                                                 (int64_t)n_vertices, 0, end_bit, s));
+    slot_counts_kernel<<<blocks_for(n_vertices), TPB, 0, s>>>(n_vertices, offsets, slot_vertex, counts);
+    TXB_CUDA_TRY(cudaGetLastError());
+  }
+  TXB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(temp, temp_b, counts, slot_offsets, (int64_t)(n_vertices + 1), s));
+  if (n_vertices > 0 && n_entries > 0) {
+    slot_copy_kernel<<<blocks_for(n_vertices), TPB, 0, s>>>(n_vertices, offsets, incidence, slot_vertex,
+                                                             slot_offsets, slot_incidence);
+    TXB_CUDA_TRY(cudaGetLastError());
+  }
   return TXB_OK;
 }
 

@@ -21,6 +21,9 @@ Data path per rank (all on the device, nothing allocated by the library):
   3. exchange: all_to_all_single(buf[recv], packed) (NCCL over NVLink; gloo on CPU)
   4. assemble: owned residual = CSR chain over [own rows, received rows]
                                                      (txb_scatter_add)
+     The owned vertices are listed in SLOT order (first own element row
+     ascending), so the assembly reads the element rows in memory order;
+     the ids come back with the residual.
 The plan (ownership, send lists, CSR) is computed once per mesh and
 partition on the host from the connectivity; every rank derives the same
 plan independently, so no metadata is exchanged.
@@ -53,7 +56,7 @@ class HaloPlan:
     lo: int                      # owned cell range [lo, hi)
     hi: int
     n_vertices: int              # global vertex count
-    owned: np.ndarray            # (n_owned,) global ids of the vertices this rank owns, ascending
+    owned: np.ndarray            # (n_owned,) global ids of the vertices this rank owns, in slot order
     offsets: np.ndarray          # (n_owned + 1,) int64 CSR over owned vertices
     incidence: np.ndarray        # (nnz,) int32 rows of buf, (rank, cell) ascending per vertex
     send_rows: np.ndarray        # (n_send,) int64 local rows owed to lower ranks, peers ascending
@@ -131,6 +134,18 @@ def build_halo_plan(cells: np.ndarray, n_vertices: int, rank: int, world: int, a
         base += sel.size
     if rows.size and rows.max() >= 2 ** 31:
         raise ValueError("halo plan rows exceed the int32 incidence range")
+    # Slot order: visit the owned vertices by their first row (always one of
+    # this rank's own element rows, in cell order) so that neighbouring
+    # assembly threads read neighbouring element rows (mesh.build_scatter_order;
+    # the reference's 3D unit mesh numbers vertices and cells in different
+    # orders).  Each chain is moved whole, so the sums do not change.
+    if owned.size:
+        perm = np.argsort(rows[offsets[:-1]], kind="stable")
+        owned, counts = owned[perm], counts[perm]
+        new_offsets = np.zeros_like(offsets)
+        np.cumsum(counts, out=new_offsets[1:])
+        src = np.repeat(offsets[:-1][perm] - new_offsets[:-1], counts) + np.arange(rows.size, dtype=np.int64)
+        rows, offsets = rows[src], new_offsets
 
     # entries of this rank's cells owed to lower ranks, per peer in (vertex, cell) order
     ipos = np.arange(lo * n_b, hi * n_b, dtype=np.int64)

@@ -193,15 +193,37 @@ def gather_coefficients(mesh: Mesh, layout: FieldLayout, global_vec, *, cells=No
 
 @dataclass
 class VertexIncidence:
-    """vertex -> (cell*n_b + b) CSR, entries in ascending cell order (device)."""
+    """vertex -> (cell*n_b + b) CSR, entries in ascending cell order (device).
+    ``slot_*``: the same lists in slot order (vertices by first element row,
+    txb_build_scatter_order) — what the scatter walks; None = vertex order."""
 
     offsets: object
     incidence: object
     n_vertices: int
     n_cells: int
+    slot_offsets: object = None
+    slot_incidence: object = None
+    slot_vertex: object = None
 
 
-def build_incidence(mesh: Mesh, cells=None) -> VertexIncidence:
+def build_scatter_order(inc: VertexIncidence) -> VertexIncidence:
+    """Attach the slot-ordered CSR to ``inc`` (device, one sort over the vertices)."""
+    torch = _torch()
+    L = _lib.lib()
+    nv = inc.n_vertices
+    n_entries = int(inc.incidence.numel()) if inc.n_cells else 0
+    slot_offsets = torch.empty((nv + 1,), dtype=torch.int64, device="cuda")
+    slot_inc = torch.empty((max(n_entries, 1),), dtype=torch.int32, device="cuda")
+    slot_vertex = torch.empty((max(nv, 1),), dtype=torch.int32, device="cuda")
+    scratch = torch.empty((max(int(L.txb_scatter_order_scratch_bytes(nv)), 16),), dtype=torch.uint8, device="cuda")
+    _lib.check(L.txb_build_scatter_order(nv, n_entries, inc.offsets.data_ptr(), inc.incidence.data_ptr(),
+                                         slot_offsets.data_ptr(), slot_inc.data_ptr(), slot_vertex.data_ptr(),
+                                         scratch.data_ptr(), _stream_ptr(torch)), "txb_build_scatter_order")
+    inc.slot_offsets, inc.slot_incidence, inc.slot_vertex = slot_offsets, slot_inc, slot_vertex
+    return inc
+
+
+def build_incidence(mesh: Mesh, cells=None, *, slot_order: bool = True) -> VertexIncidence:
     torch = _torch()
     C = cells if cells is not None else _to_device(np.ascontiguousarray(mesh.cells, dtype=np.int64), torch)[0]
     n, n_b, nv = int(C.shape[0]), mesh.dim + 1, mesh.n_vertices
@@ -212,7 +234,8 @@ def build_incidence(mesh: Mesh, cells=None) -> VertexIncidence:
                           device="cuda")
     _lib.check(L.txb_build_incidence(n, n_b, nv, C.data_ptr(), offsets.data_ptr(), inc.data_ptr(),
                                      scratch.data_ptr(), _stream_ptr(torch)), "txb_build_incidence")
-    return VertexIncidence(offsets, inc, nv, n)
+    res = VertexIncidence(offsets, inc, nv, n)
+    return build_scatter_order(res) if slot_order else res
 
 
 def scatter_add_element_vectors(mesh: Mesh, layout: FieldLayout, elem_vecs, *, incidence=None):
@@ -226,7 +249,15 @@ def scatter_add_element_vectors(mesh: Mesh, layout: FieldLayout, elem_vecs, *, i
     e, _ = _to_device(elem_vecs, torch)
     inc = incidence if incidence is not None else build_incidence(mesh)
     out = torch.empty((mesh.n_vertices * layout.n_comp,), dtype=e.dtype, device="cuda")
-    _lib.check(_lib.lib().txb_scatter_add(e.element_size(), mesh.n_vertices, layout.n_comp,
-                                          inc.offsets.data_ptr(), inc.incidence.data_ptr(), e.data_ptr(),
-                                          out.data_ptr(), _stream_ptr(torch)), "txb_scatter_add")
+    if mesh.n_cells == 0:
+        out.zero_()
+    elif inc.slot_vertex is not None:
+        _lib.check(_lib.lib().txb_scatter_add_slots(e.element_size(), mesh.n_vertices, layout.n_comp,
+                                                    inc.slot_offsets.data_ptr(), inc.slot_incidence.data_ptr(),
+                                                    inc.slot_vertex.data_ptr(), e.data_ptr(), out.data_ptr(),
+                                                    _stream_ptr(torch)), "txb_scatter_add_slots")
+    else:
+        _lib.check(_lib.lib().txb_scatter_add(e.element_size(), mesh.n_vertices, layout.n_comp,
+                                              inc.offsets.data_ptr(), inc.incidence.data_ptr(), e.data_ptr(),
+                                              out.data_ptr(), _stream_ptr(torch)), "txb_scatter_add")
     return out.cpu().numpy() if host else out

@@ -67,6 +67,45 @@ def test_gather_and_scatter_bitwise(n_comp):
                              oracle.scatter_add(mesh.cells, e, mesh.n_vertices))
 
 
+@pytest.mark.parametrize("case", ["kuhn3d", "shuffled", "isolated", "empty_mesh"])
+@pytest.mark.parametrize("n_comp", [1, 3])
+def test_slot_order_scatter_bitwise(case, n_comp):
+    """The slot-ordered scatter (vertices visited by first element row) and the
+    vertex-ordered one give the oracle's np.add.at sums bit for bit; the slot
+    order is a permutation, each slot carries its vertex's list unchanged."""
+    from paper_1607_04245_b200.mesh import build_incidence
+
+    mesh = txb.generate_unit_simplex_mesh(3, 7)
+    cells, nv = mesh.cells, mesh.n_vertices
+    rng = np.random.default_rng(4)
+    if case == "shuffled":  # random vertex numbering and cell order
+        perm = rng.permutation(nv)
+        cells = perm[cells][rng.permutation(len(cells))]
+    elif case == "isolated":  # vertices no cell touches sit between used ones
+        cells = cells * 3 + 1
+        nv = nv * 3 + 2
+    elif case == "empty_mesh":
+        cells = cells[:0]
+    m = txb.Mesh(3, np.zeros((nv, 3)), np.ascontiguousarray(cells))
+    layout = txb.FieldLayout(n_comp)
+    cells_dev = torch.from_numpy(m.cells).cuda()
+    plain, slots = build_incidence(m, cells_dev, slot_order=False), build_incidence(m, cells_dev)
+    sv = slots.slot_vertex[:nv].cpu().numpy()
+    assert np.array_equal(np.sort(sv), np.arange(nv))
+    so, si = slots.slot_offsets.cpu().numpy(), slots.slot_incidence.cpu().numpy()
+    po, pi = plain.offsets.cpu().numpy(), plain.incidence.cpu().numpy()
+    for t in rng.choice(nv, min(nv, 200), replace=False):
+        v = sv[t]
+        assert np.array_equal(si[so[t]:so[t + 1]], pi[po[v]:po[v + 1]])
+    first = [pi[po[v]] if po[v + 1] > po[v] else np.iinfo(np.int64).max for v in sv]
+    assert all(a <= b for a, b in zip(first, first[1:]))
+    for dt in (np.float64, np.float32):
+        e = rng.standard_normal((m.n_cells, 4, n_comp)).astype(dt)
+        want = oracle.scatter_add(m.cells, e, nv)
+        assert bitwise_equal(txb.scatter_add_element_vectors(m, layout, e, incidence=slots), want)
+        assert bitwise_equal(txb.scatter_add_element_vectors(m, layout, e, incidence=plain), want)
+
+
 def test_scatter_multiplicity_oracle():
     """scatter_add(gather(one-hot)) counts cells per vertex (SPEC mesh invariants)."""
     mesh = txb.generate_unit_simplex_mesh(2, 7)

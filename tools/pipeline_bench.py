@@ -1,8 +1,9 @@
 """Per-stage timing of the mesh-level residual pipeline (next rows of SURVEY §8f)
 on one config: geometry, gather, integrate (cell arrays), fused mesh kernel with
-and without given geometry, scatter-add.  Graph-timed, 2^20 cells.
+and without given geometry, scatter-add (vertex order and slot order).
+Graph-timed, 2^20 cells unless given.
 
-python tools/pipeline_bench.py [config]
+python tools/pipeline_bench.py [config] [cells]
 """
 import json
 import sys
@@ -43,6 +44,8 @@ def main():
 
     name = sys.argv[1] if len(sys.argv) > 1 else "3d_varcoef_f64"
     dim, physics, dtype, n = bench.CONFIGS[name]
+    if len(sys.argv) > 2:
+        n = int(sys.argv[2])
     factory, aux_space = PHYSICS[physics]
     form = factory(dim)
     full = txb.generate_unit_simplex_mesh(dim, refine_for(dim, n))
@@ -56,11 +59,12 @@ def main():
     aux = txb.CellAux("p0", torch.rand((n, 1), dtype=tdt, device="cuda") + 0.5) if aux_space == "p0" else None
     rule = txb.quadrature_rule(dim, 1)
     tab = txb.tabulate(dim, rule)
-    geom64 = txb.compute_geometry(mesh, cells=cells, device_out=True)
+    geom64 = txb.compute_geometry(mesh, cells=cells, vertices=verts, device_out=True)
     geom = txb.CellGeometry(geom64.inv_jacobians.to(tdt), geom64.determinants.to(tdt))
     blocks = txb.gather_coefficients(mesh, layout, glob, cells=cells)
     out = torch.empty((n, dim + 1, form.n_comp), dtype=tdt, device="cuda")
     inc = build_incidence(mesh, cells)
+    inc_plain = build_incidence(mesh, cells, slot_order=False)
     res = {}
     res["geometry_kernel_us"] = graph_time(lambda: txb.compute_geometry(mesh, cells=cells, device_out=True)) \
         if False else None  # (syncs on the orientation flag: not graph-capturable)
@@ -68,7 +72,7 @@ def main():
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(20):
-        txb.compute_geometry(mesh, cells=cells, device_out=True)
+        txb.compute_geometry(mesh, cells=cells, vertices=verts, device_out=True)
     torch.cuda.synchronize()
     res["geometry_kernel_us(wall, incl. flag sync)"] = (time.perf_counter() - t0) / 20 * 1e6
     res["gather_us"] = graph_time(lambda: txb.gather_coefficients(mesh, layout, glob, cells=cells))
@@ -82,6 +86,8 @@ def main():
         check_orientation=False))
     resid = torch.empty(full.n_vertices * form.n_comp, dtype=tdt, device="cuda")
     res["scatter_us"] = graph_time(lambda: txb.scatter_add_element_vectors(mesh, layout, out, incidence=inc))
+    res["scatter_vertex_order_us"] = graph_time(
+        lambda: txb.scatter_add_element_vectors(mesh, layout, out, incidence=inc_plain))
     print(json.dumps({"config": name, "cells": n, **{k: (round(v, 2) if v else v) for k, v in res.items()}}))
 
 

@@ -48,6 +48,22 @@ __global__ void gather_kernel(int64_t n_out, int n_b, int n_comp, const int64_t*
   }
 }
 
+// Fixed component count: one thread per (cell, b) entry -- one connectivity
+// load, NCOMP adjacent coefficient loads, no 64-bit division per scalar.
+template <typename T, int NCOMP>
+__global__ void gather_entries_kernel(int64_t n_entries, const int64_t* __restrict__ cells,
+                                      const T* __restrict__ global, T* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_entries; i += stride) {
+    const int64_t v = __ldg(cells + i);
+    T x[NCOMP];
+#pragma unroll
+    for (int k = 0; k < NCOMP; ++k) x[k] = __ldg(global + v * NCOMP + k);
+#pragma unroll
+    for (int k = 0; k < NCOMP; ++k) out[i * NCOMP + k] = x[k];
+  }
+}
+
 // ---- scatter-add: one thread per (vertex, component), sums its incident
 // element entries in ascending (cell, b) order starting from +0, exactly the
 // sequence np.add.at applies (mesh.py:232-233).  The incidence list is read
@@ -188,7 +204,21 @@ extern "C" int txb_gather_coefficients(int dtype_bytes, int64_t n_cells, int n_b
   }
   const int64_t n_out = n_cells * n_b * n_comp;
   cudaStream_t s = (cudaStream_t)stream;
-  if (dtype_bytes == 8)
+  if ((dtype_bytes == 4 || dtype_bytes == 8) && n_comp <= 3) {
+    const int64_t n_e = n_cells * n_b;
+#define TXB_GATHER(T, NC) \
+  gather_entries_kernel<T, NC><<<blocks_for(n_e), TPB, 0, s>>>(n_e, cells, (const T*)global, (T*)out)
+    if (dtype_bytes == 8) {
+      if (n_comp == 1) TXB_GATHER(double, 1);
+      else if (n_comp == 2) TXB_GATHER(double, 2);
+      else TXB_GATHER(double, 3);
+    } else {
+      if (n_comp == 1) TXB_GATHER(float, 1);
+      else if (n_comp == 2) TXB_GATHER(float, 2);
+      else TXB_GATHER(float, 3);
+    }
+#undef TXB_GATHER
+  } else if (dtype_bytes == 8)
     gather_kernel<double><<<blocks_for(n_out), TPB, 0, s>>>(n_out, n_b, n_comp, cells,
                                                             (const double*)global, (double*)out);
   else if (dtype_bytes == 4)

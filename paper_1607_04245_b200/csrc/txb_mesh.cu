@@ -12,6 +12,9 @@
 #include "txb_common.cuh"
 
 #include <algorithm>
+#include <atomic>
+#include <mutex>
+#include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
@@ -163,24 +166,38 @@ __global__ void iota_keys_kernel(int64_t n, const int64_t* __restrict__ cells, i
 // ---- geometry: one thread per cell, float64, the reference's expression
 // order (numpy evaluates a*b - c*d as two rounded products and a rounded
 // difference; the 3x3 determinant sums left to right).
+// One thread per cell; the CTA stages its cells' inverse Jacobians in shared
+// memory (odd stride D*D) and stores them as one contiguous coalesced run.
 template <int D>
-__global__ void geometry_kernel(int64_t n, const double* __restrict__ X_, const int64_t* __restrict__ cells,
-                                double* __restrict__ inv_j, double* __restrict__ det_j,
-                                unsigned long long* bad) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += stride) {
-    const int64_t* cv = cells + c * (D + 1);
-    double X[D + 1][D];
+__global__ void __launch_bounds__(TPB) geometry_kernel(int64_t n, const double* __restrict__ X_,
+                                                       const int64_t* __restrict__ cells,
+                                                       double* __restrict__ inv_j, double* __restrict__ det_j,
+                                                       unsigned long long* bad) {
+  constexpr int DD = D * D;
+  __shared__ double s_inv[TPB * DD];
+  for (int64_t base = (int64_t)blockIdx.x * TPB; base < n; base += (int64_t)gridDim.x * TPB) {
+    const int64_t c = base + threadIdx.x;
+    if (c < n) {
+      const int64_t* cv = cells + c * (D + 1);
+      int64_t ids[D + 1];
 #pragma unroll
-    for (int b = 0; b <= D; ++b)
+      for (int b = 0; b <= D; ++b) ids[b] = __ldg(cv + b);
+      double X[D + 1][D];
 #pragma unroll
-      for (int i = 0; i < D; ++i) X[b][i] = X_[cv[b] * D + i];
-    double inv[D * D], det;
-    affine_inverse<D>(X, inv, det);
+      for (int b = 0; b <= D; ++b)
 #pragma unroll
-    for (int i = 0; i < D * D; ++i) inv_j[c * D * D + i] = inv[i];
-    det_j[c] = det;
-    if (det <= 0.0) atomicMin(bad, (unsigned long long)c);
+        for (int i = 0; i < D; ++i) X[b][i] = __ldg(X_ + ids[b] * D + i);
+      double inv[DD], det;
+      affine_inverse<D>(X, inv, det);
+#pragma unroll
+      for (int i = 0; i < DD; ++i) s_inv[threadIdx.x * DD + i] = inv[i];
+      det_j[c] = det;
+      if (det <= 0.0) atomicMin(bad, (unsigned long long)c);
+    }
+    __syncthreads();
+    const int cnt = (n - base < TPB ? (int)(n - base) : TPB) * DD;
+    for (int i = threadIdx.x; i < cnt; i += TPB) inv_j[base * DD + i] = s_inv[i];
+    __syncthreads();
   }
 }
 
@@ -411,6 +428,32 @@ extern "C" int txb_build_scatter_order(int64_t n_vertices, int64_t n_entries, co
   return TXB_OK;
 }
 
+// Orientation flags of txb_compute_geometry: a static device array (slots
+// rotate, so concurrent calls on different streams do not share one) instead
+// of an allocation per call.
+constexpr int GEOM_FLAGS = 256;
+__device__ unsigned long long g_geom_flags[GEOM_FLAGS];
+
+static unsigned long long* geometry_flag() {
+  static std::mutex mu;
+  static std::vector<unsigned long long*> cache;
+  static std::atomic<uint32_t> seq{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  unsigned long long* base;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if ((int)cache.size() <= dev) cache.resize(dev + 1, nullptr);
+    if (!cache[dev]) {
+      void* p = nullptr;
+      if (cudaGetSymbolAddress(&p, g_geom_flags) != cudaSuccess) return nullptr;
+      cache[dev] = (unsigned long long*)p;
+    }
+    base = cache[dev];
+  }
+  return base + seq.fetch_add(1) % GEOM_FLAGS;
+}
+
 extern "C" int txb_compute_geometry(int dim, int64_t n_cells, const double* vertices, const int64_t* cells,
                                     double* inv_j, double* det_j, int64_t* bad_cell, void* stream) {
   if (dim != 2 && dim != 3) {
@@ -428,8 +471,8 @@ extern "C" int txb_compute_geometry(int dim, int64_t n_cells, const double* vert
     return TXB_E_ARG;
   }
   cudaStream_t s = (cudaStream_t)stream;
-  unsigned long long* flag = nullptr;
-  TXB_CUDA_TRY(cudaMallocAsync((void**)&flag, sizeof(unsigned long long), s));
+  unsigned long long* flag = geometry_flag();
+  if (!flag) return cuda_fail(cudaGetLastError(), "cudaGetSymbolAddress(g_geom_flags)");
   TXB_CUDA_TRY(cudaMemsetAsync(flag, 0xff, sizeof(unsigned long long), s));
   if (dim == 2)
     geometry_kernel<2><<<blocks_for(n_cells), TPB, 0, s>>>(n_cells, vertices, cells, inv_j, det_j, flag);
@@ -438,7 +481,6 @@ extern "C" int txb_compute_geometry(int dim, int64_t n_cells, const double* vert
   TXB_CUDA_TRY(cudaGetLastError());
   unsigned long long h = ~0ull;
   TXB_CUDA_TRY(cudaMemcpyAsync(&h, flag, sizeof(h), cudaMemcpyDeviceToHost, s));
-  TXB_CUDA_TRY(cudaFreeAsync(flag, s));
   TXB_CUDA_TRY(cudaStreamSynchronize(s));
   if (h != ~0ull) {
     if (bad_cell) *bad_cell = (int64_t)h;

@@ -183,6 +183,64 @@ def test_host_path_pinned_zero_copy(physics, fc, am):
         assert bitwise_equal(out2, want)
 
 
+def test_concurrent_callers_thread_pool():
+    """The reference runs its compiled lane from a ThreadPoolExecutor on
+    disjoint out slices (executor.py:228-239).  Eight threads at once — device
+    calls on their own streams over disjoint slices of one output, host-buffer
+    calls (staged and pinned zero-copy) on private buffers, a run-time compiled
+    form — each result bit-identical to the oracle."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    B, D, W = oracle.p1_tables(3)
+    n = 160_000
+    full, inv, det, coeffs, aux = oracle.workload(3, "varcoef_p0", n, seed=11)
+    want = oracle.integrate(1, 1, B, D, W, inv, det, coeffs, aux, np.float64)
+    dev = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (inv, det, coeffs, aux)]
+    out_dev = torch.full(tuple(coeffs.shape), float("nan"), dtype=torch.float64, device="cuda")
+    bounds = np.linspace(0, n, 5).astype(int)
+    jit = backend.jit_kernel(txb.poisson_varcoef_form(3), 1, CellAux("p0", aux))  # the shipped form's source
+    torch.cuda.synchronize()
+
+    def device_slice(i):
+        lo, hi = bounds[i], bounds[i + 1]
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            backend.run_cuda((1, 1), B, D, W, dev[0][lo:hi], dev[1][lo:hi], dev[2][lo:hi],
+                             CellAux("p0", dev[3][lo:hi]), out_dev[lo:hi], stream=s)
+        s.synchronize()
+
+    def host_call(pinned):
+        def h(a):
+            if not pinned:
+                return np.ascontiguousarray(a)
+            t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+            t.copy_(torch.from_numpy(np.ascontiguousarray(a)))
+            return t.numpy()
+        out = h(np.full(coeffs.shape, np.nan))
+        backend.run_cuda((1, 1), B, D, W, h(inv), h(det), h(coeffs), CellAux("p0", h(aux)), out)
+        return out
+
+    def jit_call():
+        out = torch.full(tuple(coeffs.shape), float("nan"), dtype=torch.float64, device="cuda")
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            backend.run_cuda(jit, B, D, W, dev[0], dev[1], dev[2], CellAux("p0", dev[3]), out, stream=s)
+        s.synchronize()
+        return out.cpu().numpy()
+
+    with ThreadPoolExecutor(8) as ex:
+        futs = [ex.submit(device_slice, i) for i in range(4)]
+        hosts = [ex.submit(host_call, p) for p in (False, True, False)]
+        jits = [ex.submit(jit_call)]
+        for f in futs:
+            f.result()
+        results = [f.result() for f in hosts + jits]
+    torch.cuda.synchronize()
+    assert bitwise_equal(out_dev.cpu().numpy(), want)
+    for r in results:
+        assert bitwise_equal(r, want)
+
+
 def test_output_fully_overwritten_and_inputs_untouched():
     B, D, W = oracle.p1_tables(2)
     full, inv, det, coeffs, aux = oracle.workload(2, "elasticity", 10_000, seed=4)

@@ -183,6 +183,29 @@ def test_fused_mesh_kernel_unaligned_connectivity():
     assert bitwise_equal(out.cpu().numpy(), ref)
 
 
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("offset", [0, 1])
+def test_fused_mesh_kernel_elasticity_coefficient_alignment(dim, dtype, offset):
+    """Given geometry, elasticity: the coefficient gathers pair a vertex's
+    components (16/8-byte loads, even and odd vertices) when the global vector
+    is pair-aligned, scalar loads when it is not — same bits either way."""
+    mesh, form, glob, aux = _mesh_problem(dim, 6 if dim == 3 else 20, txb.elasticity_form, None, seed=21 + dim)
+    rule = txb.quadrature_rule(dim, 1)
+    npdt = np.float64 if dtype == "f64" else np.float32
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    tab = txb.tabulate(dim, rule)
+    inv, det = oracle.geometry(mesh.vertices, mesh.cells)
+    ref = oracle.integrate(2, 0, tab.basis, tab.basis_der, rule.weights, inv, det,
+                           oracle.gather(mesh.cells, glob, dim), None, npdt)
+    buf = torch.empty(glob.size + offset, dtype=tdt, device="cuda")
+    g = buf[offset:]
+    g.copy_(torch.from_numpy(glob.astype(npdt)))
+    geom = txb.CellGeometry(torch.from_numpy(inv.astype(npdt)).cuda(), torch.from_numpy(det.astype(npdt)).cuda())
+    out = txb.integrate_mesh(mesh, txb.FieldLayout(dim), tab, rule, form, g, None, dtype=dtype, cell_geom=geom)
+    assert bitwise_equal(out.cpu().numpy(), ref)
+
+
 def test_fused_mesh_kernel_orientation_error():
     mesh = txb.Mesh(3, np.array([[0.0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [0, 0, -1]]),
                     np.array([[0, 1, 2, 3], [0, 1, 2, 4]]))

@@ -11,10 +11,17 @@
 //     txfem/codegen.py:215-221), inlined;
 //   * any number of auxiliary fields (TXB_NAUX), P0 or P1, with the P1
 //     gradient when the form asks for it (txfem/_kernels_py.py:93-110);
-//   * any tabulation (no standard-P1 shortcuts): every chain starts at +0 and
-//     runs in the numpy lane's order (txfem/_kernels_py.py:20-90), so the
-//     element vectors are bit-identical to the reference's python lane for
-//     sources that evaluate like their f1_many / f0_many.
+//   * any tabulation: every chain starts at +0 and runs in the numpy lane's
+//     order (txfem/_kernels_py.py:20-90), so the element vectors are
+//     bit-identical to the reference's python lane for sources that evaluate
+//     like their f1_many / f0_many.  Two entry points share the source:
+//     txb_jit_integrate (any D table) and txb_jit_integrate_std (the standard
+//     P1 table, chosen by the host when D is bitwise that table): there the
+//     pulled-back gradients are T[0] = -invJ[0] - invJ[1] (- invJ[2]) and
+//     T[b>=1] = invJ row b-1 -- the same values as the full chain up to the
+//     sign of zero, which the +0-started consumer chains (grad u, grad a and
+//     the basis-phase sums) absorb -- and only T[0] goes through the exchange
+//     area (the basis phase reads the invJ rows from the stage).
 //
 // The including unit defines: real, TXB_DIM, TXB_NQ, TXB_NCOMP, TXB_NAUX,
 // TXB_AUX_MODE (0 none, 1 P0, 2 P1), TXB_HAS_F0, TXB_GRAD_A, TXB_F1 and, with
@@ -39,21 +46,25 @@ constexpr int S = (int)sizeof(real);
 // consecutive words; the basis-phase loads (lanes = (cell, b, c)) spread over
 // the banks (the cell-major odd stride left 4-way conflicts on the T loads).
 constexpr int P = CW + 4;
-constexpr int NTR = NQ * NB * D, NF1 = NQ * NCOMP * D, NF0 = HAS_F0 ? NQ * NCOMP : 0;
-constexpr int SCRATCH_BYTES = round_up(P * (NTR + NF1 + NF0) * S, 16);
+constexpr int NF1 = NQ * NCOMP * D, NF0 = HAS_F0 ? NQ * NCOMP : 0;
+template <bool STD>
+struct Area {
+  static constexpr int NTR = STD ? D : NQ * NB * D;  // rows of T in the exchange area
+  static constexpr int BYTES = round_up(P * (NTR + NF1 + NF0) * S, 16);
+};
 
 __device__ __forceinline__ int inv_bytes(int n) { return round_up(n * DD * S, 16); }
 __device__ __forceinline__ int det_bytes(int n) { return round_up(n * S, 16); }
 __device__ __forceinline__ int coef_bytes(int n) { return round_up(n * NBC * S, 16); }
 __device__ __forceinline__ int aux_bytes(int n) { return round_up(n * AUXW * S, 16); }
 
-template <bool VEC>
+template <bool STD, bool VEC>
 __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const real* __restrict__ s_inv,
                                            const real* __restrict__ s_det, const real* __restrict__ s_coef,
                                            const real* __restrict__ s_aux, real* __restrict__ scratch, int c0,
                                            int ncell, real* __restrict__ out, int lane) {
   real* s_tr = scratch;
-  real* s_f1 = s_tr + P * NTR;
+  real* s_f1 = s_tr + P * Area<STD>::NTR;
   real* s_f0 = s_f1 + P * NF1;
   const int nc = min(CW, ncell - c0);
 
@@ -70,16 +81,31 @@ __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const re
 
     // pulled-back gradients T[b][k] = sum_j D[q][b][j] invJ[j][k]  (_kernels_py.py:78-90)
     real tr[NB][D];
-#pragma unroll
-    for (int b = 0; b < NB; ++b)
+    if constexpr (STD) {
 #pragma unroll
       for (int k = 0; k < D; ++k) {
-        real acc = real(0);
+        real acc = -J[k];
 #pragma unroll
-        for (int j = 0; j < D; ++j) acc = add(acc, mul(tab.D[(q * NB + b) * D + j], J[j * D + k]));
-        tr[b][k] = acc;
-        s_tr[((q * NB + b) * D + k) * P + lc] = acc;
+        for (int j = 1; j < D; ++j) acc = add(acc, -J[j * D + k]);
+        tr[0][k] = acc;
+        if (q == 0) s_tr[k * P + lc] = acc;
       }
+#pragma unroll
+      for (int b = 1; b < NB; ++b)
+#pragma unroll
+        for (int k = 0; k < D; ++k) tr[b][k] = J[(b - 1) * D + k];
+    } else {
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          real acc = real(0);
+#pragma unroll
+          for (int j = 0; j < D; ++j) acc = add(acc, mul(tab.D[(q * NB + b) * D + j], J[j * D + k]));
+          tr[b][k] = acc;
+          s_tr[((q * NB + b) * D + k) * P + lc] = acc;
+        }
+    }
 
     // u and grad u at the point (_kernels_py.py:44-51)
     real u[NCOMP];
@@ -149,12 +175,27 @@ __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const re
     const int b = r / NCOMP;
     const int c = r - b * NCOMP;
     real e = real(0);  // _kernels_py.py:67-75: q-major, f0 term then the k terms
+    if constexpr (STD) {
+      // T[0] from the exchange area, T[b>=1] = invJ row b-1 (stage, or global on the direct path)
+      real t[D];
+      const real* tp = b == 0 ? s_tr + ec : s_inv + (c0 + ec) * DD + (b - 1) * D;
+      const int step = b == 0 ? P : 1;
 #pragma unroll
-    for (int qq = 0; qq < NQ; ++qq) {
-      if constexpr (HAS_F0) e = add(e, mul(tab.B[qq * NB + b], s_f0[(qq * NCOMP + c) * P + ec]));
+      for (int k = 0; k < D; ++k) t[k] = tp[k * step];
 #pragma unroll
-      for (int k = 0; k < D; ++k)
-        e = add(e, mul(s_tr[((qq * NB + b) * D + k) * P + ec], s_f1[((qq * NCOMP + c) * D + k) * P + ec]));
+      for (int qq = 0; qq < NQ; ++qq) {
+        if constexpr (HAS_F0) e = add(e, mul(tab.B[qq * NB + b], s_f0[(qq * NCOMP + c) * P + ec]));
+#pragma unroll
+        for (int k = 0; k < D; ++k) e = add(e, mul(t[k], s_f1[((qq * NCOMP + c) * D + k) * P + ec]));
+      }
+    } else {
+#pragma unroll
+      for (int qq = 0; qq < NQ; ++qq) {
+        if constexpr (HAS_F0) e = add(e, mul(tab.B[qq * NB + b], s_f0[(qq * NCOMP + c) * P + ec]));
+#pragma unroll
+        for (int k = 0; k < D; ++k)
+          e = add(e, mul(s_tr[((qq * NB + b) * D + k) * P + ec], s_f1[((qq * NCOMP + c) * D + k) * P + ec]));
+      }
     }
     o_base[o] = e;
   };
@@ -168,16 +209,9 @@ __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const re
   __syncwarp();  // scratch is reused by the next slice
 }
 
-}  // namespace jit
-}  // namespace txb
-
-// dynamic-scheduling counters of this module (zero at load, self-resetting)
-__device__ unsigned long long txb_jit_work_pool[4096][2];
-
-extern "C" __global__ void __launch_bounds__(txb::MAX_CTA_THREADS, 1)
-txb_jit_integrate(const __grid_constant__ txb::IntegrateArgs<real> a) {
-  using namespace txb;
-  using namespace txb::jit;
+template <bool STD>
+__device__ __forceinline__ void integrate_body(const IntegrateArgs<real>& a) {
+  constexpr int SCRATCH_BYTES = Area<STD>::BYTES;
   extern __shared__ __align__(128) unsigned char smem[];
   const int nbc = a.n_bc;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -226,13 +260,29 @@ txb_jit_integrate(const __grid_constant__ txb::IntegrateArgs<real> a) {
       const real* s_coef = reinterpret_cast<const real*>(st + o_coef);
       const real* s_aux = reinterpret_cast<const real*>(st + o_aux);
       for (int c = warp * CW; c < ncell; c += W * CW)
-        warp_slice<true>(a.tab, s_inv, s_det, s_coef, s_aux, scratch, c, ncell, out, lane);
+        warp_slice<STD, true>(a.tab, s_inv, s_det, s_coef, s_aux, scratch, c, ncell, out, lane);
     } else {
       // unaligned caller buffers or an odd-sized partial batch: straight from global memory
       const real* g_aux = AUXW ? a.aux + c0 * AUXW : nullptr;
       for (int c = warp * CW; c < ncell; c += W * CW)
-        warp_slice<false>(a.tab, a.inv_j + c0 * DD, a.det_j + c0, a.coeffs + c0 * NBC, g_aux, scratch, c, ncell,
+        warp_slice<STD, false>(a.tab, a.inv_j + c0 * DD, a.det_j + c0, a.coeffs + c0 * NBC, g_aux, scratch, c, ncell,
                           out, lane);
     }
   });
+}
+
+}  // namespace jit
+}  // namespace txb
+
+// dynamic-scheduling counters of this module (zero at load, self-resetting)
+__device__ unsigned long long txb_jit_work_pool[4096][2];
+
+extern "C" __global__ void __launch_bounds__(txb::MAX_CTA_THREADS, 1)
+txb_jit_integrate(const __grid_constant__ txb::IntegrateArgs<real> a) {
+  txb::jit::integrate_body<false>(a);
+}
+
+extern "C" __global__ void __launch_bounds__(txb::MAX_CTA_THREADS, 1)
+txb_jit_integrate_std(const __grid_constant__ txb::IntegrateArgs<real> a) {
+  txb::jit::integrate_body<true>(a);
 }

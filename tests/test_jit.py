@@ -215,6 +215,40 @@ def test_shipped_forms_jit_equals_ahead_of_time_kernel(dim, physics):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("name", SPECS)
+@pytest.mark.parametrize("dim", [2, 3])
+def test_jit_standard_table_entry_point_matches_generic(name, dim, monkeypatch):
+    """The standard-P1-table entry point (txb_jit_integrate_std: T[0] = -sum of
+    invJ rows, T[b] = invJ rows) and the generic one give the oracle's bits on
+    a structured mesh, whose inverse Jacobians are full of exact +-0 (the sign
+    of zero is where the two pull-backs may differ), midpoint and two-point
+    rules, both precisions."""
+    s = user_forms.spec(name, dim)
+    f = form_of(name, dim)
+    mesh = txb.generate_unit_simplex_mesh(dim, 14 if dim == 2 else 5)
+    inv, det = oracle.geometry(mesh.vertices, mesh.cells)
+    assert (inv == 0).mean() > 0.2
+    n = mesh.n_cells
+    rng = np.random.default_rng(17)
+    co = rng.standard_normal((n, dim + 1, f.n_comp))
+    co[::7] = 0.0  # zero coefficient blocks: signed-zero products in grad u
+    aux = aux_for(s, n, rng)
+    for rule in (txb.quadrature_rule(dim, 1), txb.two_point_rule(dim)):
+        tab = txb.tabulate(dim, rule)
+        for dt in (np.float64, np.float32):
+            k = txb.jit_kernel(f, rule.n_q, aux, np.dtype(dt).itemsize)
+            want = oracle.integrate_forms(s["f1_many"], s["f0_many"], s["uses_grad_a"], s["aux"], tab.basis,
+                                          tab.basis_der, rule.weights, inv, det, co,
+                                          None if aux is None else aux.values, dt)
+            monkeypatch.setenv("TXB_DISABLE_STD", "0")
+            std = _run(k, tab.basis, tab.basis_der, rule.weights, inv, det, co, aux, dt)
+            monkeypatch.setenv("TXB_DISABLE_STD", "1")
+            gen = _run(k, tab.basis, tab.basis_der, rule.weights, inv, det, co, aux, dt)
+            assert bitwise_equal(std, want), (rule.n_q, dt)
+            assert bitwise_equal(gen, want), (rule.n_q, dt)
+
+
+@pytest.mark.gpu
 def test_integrate_transposed_with_a_user_form():
     """Mesh-level driver: geometry -> gather -> run-time compiled integration ->
     deterministic scatter-add (executor.py:161-267) for the reaction form."""

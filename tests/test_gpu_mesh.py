@@ -235,3 +235,48 @@ def test_fused_mesh_kernel_baseline_configs_by_hash(name):
                                  torch.from_numpy(glob.astype(npdt)).cuda(), aux, dtype=dtype)
         torch.cuda.synchronize()
         assert hashlib.sha256(out.cpu().numpy().tobytes()).hexdigest() == e[key], (name, dtype)
+
+
+# ---- randomised mesh-level residuals (integrate_transposed end to end) ----
+
+from hypothesis import HealthCheck, given, settings, strategies as st  # noqa: E402
+
+
+@settings(max_examples=30, deadline=None, suppress_health_check=list(HealthCheck))
+@given(dim=st.integers(2, 3), refine=st.integers(1, 9), form_i=st.integers(0, 3), dtype=st.sampled_from(["f64", "f32"]),
+       given_geom=st.booleans(), two_point=st.booleans(), seed=st.integers(0, 2 ** 31 - 1))
+def test_random_mesh_residual_bitwise(dim, refine, form_i, dtype, given_geom, two_point, seed):
+    """integrate_transposed on a Kuhn mesh with a random vertex numbering and
+    cell order (the gathers, the slot order and the incidence see arbitrary
+    index patterns): fused mesh kernel (in-kernel or given geometry) +
+    slot-ordered scatter-add, bit-identical to the oracle's geometry -> gather
+    -> integrate -> np.add.at."""
+    rng = np.random.default_rng(seed)
+    base = txb.generate_unit_simplex_mesh(dim, refine if dim == 3 else 3 * refine)
+    perm = rng.permutation(base.n_vertices)
+    inv_perm = np.argsort(perm)
+    verts = np.ascontiguousarray(base.vertices[inv_perm])  # new vertex i = old vertex inv_perm[i]
+    cells = np.ascontiguousarray(perm[base.cells][rng.permutation(base.n_cells)])
+    mesh = txb.Mesh(dim, verts, cells)
+    factory, aux_space = FORMS[form_i]
+    form = factory(dim)
+    layout = txb.FieldLayout(form.n_comp)
+    rule = txb.two_point_rule(dim) if two_point else txb.quadrature_rule(dim, 1)
+    tab = txb.tabulate(dim, rule)
+    glob = rng.standard_normal(layout.global_size(mesh))
+    aux = None
+    if aux_space == "p0":
+        aux = txb.CellAux("p0", rng.uniform(0.5, 1.5, (mesh.n_cells, 1)))
+    elif aux_space == "p1":
+        aux = txb.CellAux("p1", rng.uniform(0.5, 1.5, (mesh.n_vertices, 1))[mesh.cells])
+    npdt = np.float64 if dtype == "f64" else np.float32
+    inv, det = oracle.geometry(mesh.vertices, mesh.cells)
+    cg = txb.CellGeometry(inv, det) if given_geom else None
+    res, _ = txb.integrate_transposed(mesh, layout, tab, rule, form, glob, aux, n_bl=8, n_cb=2, dtype=dtype,
+                                      shared_mem_limit=None, cell_geom=cg)
+    fc = {"poisson": 0, "poisson_varcoef": 1, "elasticity": 2}[form.name]
+    am = {None: 0, "p0": 1, "p1": 2}[aux_space]
+    elem = oracle.integrate(fc, am, tab.basis, tab.basis_der, rule.weights, inv, det,
+                            oracle.gather(mesh.cells, glob, form.n_comp), None if aux is None else aux.values, npdt)
+    want = oracle.scatter_add(mesh.cells, elem, mesh.n_vertices)
+    assert bitwise_equal(res, want)

@@ -29,6 +29,7 @@
 // timeout the kernel records an error in the window and finishes, so a lost
 // peer never hangs the GPU; txb_halo_window_error reports it.
 #include "txb_common.cuh"
+#include "txb_halo.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -37,46 +38,8 @@
 namespace txb {
 namespace {
 
-constexpr int MAX_RANKS = 64;
+using namespace halo;  // window layout and spin/release primitives (txb_halo.cuh)
 constexpr int TPB = 256;
-
-struct WindowHeader {
-  unsigned long long flags[MAX_RANKS];
-  unsigned long long acks[MAX_RANKS];
-  unsigned int counters[4];  // [0..1] put, [2..3] assemble, by epoch parity
-  int error;                 // 0 ok, 1 put timed out waiting for an ack, 2 assemble timed out waiting for a flag
-  int pad[3];
-};
-constexpr int64_t HEADER_BYTES = 2048;
-static_assert(sizeof(WindowHeader) <= HEADER_BYTES, "window header");
-
-__device__ __forceinline__ unsigned long long load_acquire_sys(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void store_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-__device__ __forceinline__ unsigned long long now_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-// Spin until *p >= want (acquire, system scope); false on timeout.
-__device__ bool wait_at_least(const unsigned long long* p, unsigned long long want, unsigned long long timeout_ns) {
-  const unsigned long long t0 = now_ns();
-  while (load_acquire_sys(p) < want) {
-    if (now_ns() - t0 > timeout_ns) return false;
-    __nanosleep(200);
-  }
-  return true;
-}
-
-__host__ __device__ __forceinline__ WindowHeader* header(void* w) { return reinterpret_cast<WindowHeader*>(w); }
 
 template <typename T>
 __global__ void __launch_bounds__(TPB)
@@ -180,11 +143,7 @@ assemble_kernel(int64_t n_owned, const int64_t* __restrict__ offsets, const int3
   }
 }
 
-unsigned long long timeout_ns() {
-  const char* v = std::getenv("TXB_HALO_TIMEOUT_MS");
-  const long long ms = v && *v ? std::atoll(v) : 10000;
-  return (unsigned long long)std::max(1LL, ms) * 1000000ull;
-}
+
 
 int grid_for(int64_t n, int sms_cap = 4 * 148) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((n + TPB - 1) / TPB, sms_cap));

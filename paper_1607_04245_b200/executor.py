@@ -179,6 +179,7 @@ def _mesh_on_device(mesh: Mesh, torch):
 
 
 _PART_CACHE: dict = {}
+_PART_CACHE_SIZE = 8
 
 
 def _partition_on_device(mesh: Mesh, lo: int, hi: int, torch):
@@ -190,7 +191,8 @@ def _partition_on_device(mesh: Mesh, lo: int, hi: int, torch):
         return hit[2], hit[3]
     cells = torch.from_numpy(np.ascontiguousarray(mesh.cells[lo:hi], dtype=np.int64)).to("cuda")
     verts = torch.from_numpy(np.ascontiguousarray(mesh.vertices, dtype=np.float64)).to("cuda")
-    _PART_CACHE.clear()
+    while len(_PART_CACHE) >= _PART_CACHE_SIZE:  # several ranks may share a process (peer-group emulation)
+        _PART_CACHE.pop(next(iter(_PART_CACHE)))
     _PART_CACHE[key] = (mesh.cells, mesh.vertices, cells, verts)
     return cells, verts
 

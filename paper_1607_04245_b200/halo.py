@@ -272,9 +272,15 @@ class PeerHalo:
         self.n_out, self.n_in = int(out_peers.size), int(in_peers.size)
         self.my_slot = slot_bytes(plan.n_recv, n_comp, dtype_bytes)
 
+    def _check_rows(self, rows):
+        plan, nc, s = self.plan, self.n_comp, self.dtype_bytes
+        if tuple(rows.shape) != (plan.n_local_rows, nc) or rows.element_size() != s or not rows.is_contiguous():
+            raise ValueError(f"rows must be a contiguous ({plan.n_local_rows}, {nc}) tensor of {s}-byte scalars")
+
     def exchange_assemble(self, rows):
         """rows: CUDA tensor (n_local_rows, n_comp) — this rank's element rows.
-        Returns the owned-vertex residual (n_owned, n_comp).  Asynchronous."""
+        Put (txb_halo_put) then assemble.  Returns the owned-vertex residual
+        (n_owned, n_comp).  Asynchronous."""
         import ctypes
 
         import torch
@@ -282,17 +288,33 @@ class PeerHalo:
         from . import _lib
 
         plan, nc, s = self.plan, self.n_comp, self.dtype_bytes
-        if tuple(rows.shape) != (plan.n_local_rows, nc) or rows.element_size() != s or not rows.is_contiguous():
-            raise ValueError(f"rows must be a contiguous ({plan.n_local_rows}, {nc}) tensor of {s}-byte scalars")
+        self._check_rows(rows)
         self.epoch += 1
         d = self._d
-        dc = plan.device_arrays(torch)
         L = _lib.lib()
         stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
         ptr = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
         _lib.check(L.txb_halo_put(s, nc, plan.rank, plan.world, plan.n_send, ptr(d["send_rows"]), ptr(d["send_peer"]),
                                   ptr(d["send_dst"]), ptr(rows), ptr(d["windows"]), ptr(d["slot_bytes"]),
                                   ptr(d["out_peers"]), self.n_out, self.epoch, stream), "txb_halo_put")
+        return self.assemble(rows)
+
+    def assemble(self, rows):
+        """The assembly half of the current epoch (its put already issued by
+        exchange_assemble).  Returns the owned-vertex residual (n_owned, n_comp)."""
+        import ctypes
+
+        import torch
+
+        from . import _lib
+
+        plan, nc, s = self.plan, self.n_comp, self.dtype_bytes
+        self._check_rows(rows)
+        d = self._d
+        dc = plan.device_arrays(torch)
+        L = _lib.lib()
+        stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        ptr = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
         out = torch.empty((max(plan.owned.size, 1), nc), dtype=rows.dtype, device=rows.device)
         _lib.check(L.txb_halo_assemble(s, nc, plan.rank, plan.world, plan.owned.size, ptr(dc["offsets"]),
                                        ptr(dc["incidence"]), plan.n_local_rows, ptr(rows), ptr(d["windows"]),

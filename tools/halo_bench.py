@@ -2,6 +2,7 @@
 (NCCL all_to_all vs the peer-memory windows), device time max over ranks.
 
   python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 tools/halo_bench.py [cells_per_gpu]
+  python tools/halo_bench.py --local W [cells_per_rank]   (W emulated ranks in one process on one GPU)
 
 One process per GPU of one node.  Each rank owns a contiguous range of a
 Kuhn mesh of N x cells_per_gpu tetrahedra (3D var-coef f64), integrates it
@@ -89,5 +90,58 @@ def main():
     dist.destroy_process_group()
 
 
+def local(world, per_rank):
+    """All ranks in this process on one stream (highest rank first), peer
+    windows in device memory: the summed device time of one residual over all
+    ranks (integration + put + assembly per rank), the gathered residual
+    checked bitwise across repeats."""
+    import torch
+
+    import paper_1607_04245_b200 as txb
+    from paper_1607_04245_b200 import halo
+    from paper_1607_04245_b200.workload import refine_for
+
+    dim = 3
+    full = txb.generate_unit_simplex_mesh(dim, refine_for(dim, per_rank * world))
+    mesh = txb.Mesh(dim, full.vertices, np.ascontiguousarray(full.cells[:per_rank * world]))
+    form, layout = txb.poisson_varcoef_form(dim), txb.FieldLayout(1)
+    rule = txb.quadrature_rule(dim, 1)
+    tab = txb.tabulate(dim, rule)
+    glob = torch.from_numpy(np.random.default_rng(1).standard_normal(mesh.n_vertices)).cuda()
+    aux = txb.CellAux("p0", torch.from_numpy(np.random.default_rng(2).uniform(0.5, 1.5, (mesh.n_cells, 1))).cuda())
+    plans = [halo.build_halo_plan(mesh.cells, mesh.n_vertices, r, world) for r in range(world)]
+    group = halo.local_peer_group(plans, 1, 8)
+
+    def residual():
+        return [txb.integrate_partitioned(mesh, layout, tab, rule, form, glob, aux, rank=r, world=world,
+                                          peer=group[r]) for r in reversed(range(world))]
+
+    ref = None
+    for _rep in range(2):
+        for _ in range(3):
+            residual()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            outs = residual()
+        e1.record()
+        torch.cuda.synchronize()
+        for g in group:
+            g.check()
+        got = np.zeros(mesh.n_vertices)
+        for ids, res, _ in outs:
+            got[ids] = res.cpu().numpy()
+        ref = got if ref is None else ref
+        print(json.dumps({"mode": "local", "world": world, "cells_per_rank": per_rank,
+                          "ms_per_residual_all_ranks": e0.elapsed_time(e1) / 10,
+                          "rows_sent_per_rank": [int(p.n_send) for p in plans],
+                          "same_bits": got.tobytes() == ref.tobytes()}), flush=True)
+    group[0].close()
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "--local":
+        local(int(sys.argv[2]), int(sys.argv[3]) if len(sys.argv) > 3 else 1 << 20)
+    else:
+        main()

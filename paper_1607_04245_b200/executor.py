@@ -317,10 +317,10 @@ def integrate_partitioned(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule
     partition over ``world`` ranks (shard.cell_range): integrate the rank's
     cells on its GPU, then the halo exchange + assembly of halo.py.
 
-    Returns (owned_vertex_ids (numpy), owned_residual (CUDA tensor
-    (n_owned * n_comp,)), plan).  Concatenating every rank's owned entries
-    reproduces the reference residual (executor.py:266, np.add.at order) bit
-    for bit.  ``exchange``: halo.all_to_all_exchange() under torch.distributed
+    Returns (owned_vertex_ids (numpy, in the plan's slot order),
+    owned_residual (CUDA tensor (n_owned * n_comp,)), plan).  Placing every
+    rank's owned entries at their vertex ids reproduces the reference
+    residual (executor.py:266, np.add.at order) bit for bit.  ``exchange``: halo.all_to_all_exchange() under torch.distributed
     (None for world == 1).  ``plan``: a cached halo.build_halo_plan result.
     ``peer``: a halo.PeerHalo — the exchange over peer memory (txb_halo_put /
     txb_halo_assemble) instead of ``exchange``; its plan is used."""

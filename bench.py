@@ -379,6 +379,24 @@ def api_rows(steps=20):
                          "vertices": mesh.n_vertices, "ms_per_call": dt * 1e3,
                          "gcells_per_s": mesh.n_cells / dt / 1e9,
                          "path": "host numpy in/out: H2D coefficients, fused mesh kernel, scatter-add, D2H residual"})
+        # the same call with device-resident coefficients and kappa (CUDA tensors in, CUDA residual out):
+        # what a GPU-resident solver loop pays per residual; wall time incl. the orientation-flag read
+        glob_dev = torch.from_numpy(glob).cuda()
+        aux_dev = None if aux is None else txb.CellAux("p0", torch.from_numpy(aux.values).cuda())
+        for _ in range(3):
+            txb.integrate_transposed(mesh, layout, tab, rule, form, glob_dev, aux_dev, n_bl=n_bl, n_cb=8,
+                                     dtype=dtype, shared_mem_limit=None)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            res, _ = txb.integrate_transposed(mesh, layout, tab, rule, form, glob_dev, aux_dev, n_bl=n_bl, n_cb=8,
+                                              dtype=dtype, shared_mem_limit=None)
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / steps
+        rows.append({"config": f"api_integrate_transposed_device_{name}", "cells": mesh.n_cells,
+                     "vertices": mesh.n_vertices, "ms_per_call": dt * 1e3, "gcells_per_s": mesh.n_cells / dt / 1e9,
+                     "path": "CUDA tensors in/out: fused mesh kernel (in-kernel geometry) + scatter-add"})
+        del glob_dev, aux_dev
         del geom
         torch.cuda.empty_cache()
     return rows

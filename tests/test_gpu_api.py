@@ -127,3 +127,15 @@ def test_orientation_error_names_the_cell():
                     np.array([[0, 1, 2], [0, 1, 3]]))
     with pytest.raises(txb.OrientationError, match="cell 1"):
         txb.compute_geometry(mesh)
+
+
+def test_integrate_transposed_orientation_error_names_the_cell():
+    """The mesh-level call raises the reference's OrientationError for a
+    degenerate / negatively oriented cell (the in-kernel geometry's flag is
+    read once after the scatter-add is queued)."""
+    mesh = txb.Mesh(3, np.array([[0.0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [0, 0, -1], [1, 1, 1]]),
+                    np.array([[0, 1, 2, 3], [0, 1, 2, 5], [0, 1, 2, 4]]))
+    rule = txb.quadrature_rule(3, 1)
+    with pytest.raises(txb.OrientationError, match="cell 2"):
+        txb.integrate_transposed(mesh, txb.FieldLayout(1), txb.tabulate(3, rule), rule, txb.poisson_form(3),
+                                 np.ones(6), None, n_bl=4, n_cb=2, shared_mem_limit=None)

@@ -112,6 +112,7 @@ class ClockSampler:
 
     def __enter__(self):
         if self.ok:
+            self._stop = threading.Event()
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         return self
@@ -120,13 +121,20 @@ class ClockSampler:
         if self.ok:
             self._stop.set()
             self.t.join()
+        if self.in_timed is None:
+            self.in_timed = len(self.samples)
+
+    in_timed = None  # samples taken inside the timed region (the first window)
 
     def summary(self):
         if not self.ok:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
         names = [n for bit, n in self.REASONS.items() if self.reasons & bit and n != "gpu_idle"]
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
-                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples),
+                "samples_in_timed_region": self.in_timed,
+                "window": "the timed region, then replays of the same timed graph (untimed) until "
+                          ">= 0.25 s of load was sampled"}
 
 
 # ----------------------------------------------------------------------------
@@ -228,6 +236,14 @@ def time_device(wl, steps, warmup, n_sets, barrier=None, sampler=None, jit=False
                 launch(warmup + i)
         t1.record(stream)
         torch.cuda.synchronize()
+    if sampler is not None and graph is not None:
+        # a short timed region (small K) leaves few NVML samples: keep the same load
+        # running (replays of the timed graph, untimed) while sampling for >= 0.25 s
+        with sampler:
+            t_end = time.perf_counter() + 0.25
+            while time.perf_counter() < t_end:
+                graph.replay()
+                torch.cuda.synchronize()
     if barrier:
         barrier()
     total = t0.elapsed_time(t1)

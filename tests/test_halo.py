@@ -63,6 +63,35 @@ def test_plan_partitions_every_contribution(dim, refine, world, align):
         assert p.incidence.dtype == np.int32 and p.incidence.max(initial=-1) < p.n_local_rows + p.n_recv
 
 
+@pytest.mark.parametrize("world", [1, 2, 3])
+@pytest.mark.parametrize("shuffle", [False, True])
+def test_plan_slot_order(world, shuffle):
+    """Owned vertices are listed in slot order (first chain row ascending);
+    each chain is the vertex's contributions in (rank, cell, b) order — own
+    rows first, then each higher rank's received rows — whatever the vertex
+    numbering and cell order."""
+    mesh = generate_unit_simplex_mesh(3, 4)
+    cells = mesh.cells
+    if shuffle:
+        rng = np.random.default_rng(world)
+        cells = rng.permutation(mesh.n_vertices)[cells][rng.permutation(len(cells))]
+    n, n_b = cells.shape
+    for r in range(world):
+        p = halo.build_halo_plan(cells, mesh.n_vertices, r, world, 16)
+        first = p.incidence[p.offsets[:-1]]
+        assert np.all(np.diff(first) > 0)  # strictly ascending (distinct rows)
+        assert np.all(first < p.n_local_rows)  # the owner's own row comes first
+        # reference chain of every owned vertex: global incidence positions in ascending order
+        flat = cells.ravel()
+        for j in np.random.default_rng(r).choice(p.owned.size, min(60, p.owned.size), replace=False):
+            v = p.owned[j]
+            want = np.nonzero(flat == v)[0]  # (cell, b) positions, ascending = np.add.at order
+            got = p.incidence[p.offsets[j]:p.offsets[j + 1]]
+            own = want[(want >= p.lo * n_b) & (want < p.hi * n_b)] - p.lo * n_b
+            assert np.array_equal(got[:own.size], own)
+            assert got.size == want.size and np.all(got[own.size:] >= p.n_local_rows)
+
+
 def _elem(mesh, lo, hi):
     inv, det = oracle.geometry(mesh.vertices, mesh.cells[lo:hi])
     glob = np.random.default_rng(5).standard_normal(mesh.n_vertices)

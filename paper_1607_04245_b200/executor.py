@@ -29,7 +29,7 @@ import numpy as np
 from . import backend as _backend
 from .element import QuadratureRule, Tabulation
 from .errors import CapacityError, ShapeError
-from .mesh import (CellGeometry, FieldLayout, Mesh, build_incidence, compute_geometry,
+from .mesh import (CellGeometry, FieldLayout, Mesh, _stream_ptr, build_incidence, compute_geometry,
                    gather_coefficients, scatter_add_element_vectors)
 from .physics import CellAux, PhysicsForm
 from .schedule import DEFAULT_THREAD_LIMIT, ExecutionGeometry, derive_execution_geometry
@@ -77,13 +77,19 @@ def _resolve_backend(requested: Optional[str], form: PhysicsForm, n_q: int, aux,
     return kernel
 
 
+_CUDA_OK = False  # torch.cuda.is_available() seen True once (it does not flip back within a process)
+
+
 def _torch():
+    global _CUDA_OK
     import torch
 
-    if not torch.cuda.is_available():
-        from .errors import CudaLaneError
+    if not _CUDA_OK:
+        if not torch.cuda.is_available():
+            from .errors import CudaLaneError
 
-        raise CudaLaneError("the CUDA lane needs a CUDA device")
+            raise CudaLaneError("the CUDA lane needs a CUDA device")
+        _CUDA_OK = True
     return torch
 
 
@@ -246,14 +252,25 @@ def integrate_transposed(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule:
 
 
 
+_FUSABLE: dict = {}
+
+
 def _mesh_fusable(tab: Tabulation, rule: QuadratureRule) -> bool:
     """The fused mesh kernel needs the standard P1 reference gradients (what
-    element.tabulate produces for every rule) and n_q <= 2."""
+    element.tabulate produces for every rule) and n_q <= 2.  Memoised per
+    tabulation object (tables are not mutated in place)."""
     if rule.n_q > 2:
         return False
+    hit = _FUSABLE.get(id(tab))
+    if hit is not None and hit[0] is tab:
+        return hit[1]
     D = np.asarray(tab.basis_der, dtype=np.float64)
     want = np.vstack([-np.ones((1, tab.dim)), np.eye(tab.dim)])
-    return all(np.array_equal(D[q], want) for q in range(D.shape[0]))
+    ok = all(np.array_equal(D[q], want) for q in range(D.shape[0]))
+    if len(_FUSABLE) > 64:
+        _FUSABLE.clear()
+    _FUSABLE[id(tab)] = (tab, ok)
+    return ok
 
 
 def integrate_mesh(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: QuadratureRule, form: PhysicsForm,
@@ -300,7 +317,7 @@ def integrate_mesh(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: Quadr
     rc = _lib.lib().txb_integrate_mesh(
         kernel[0], kernel[1], dt.itemsize, mesh.dim, rule.n_q, form.n_comp, n, mesh.n_vertices,
         B.ctypes.data, D.ctypes.data, W.ctypes.data, X.data_ptr(), C.data_ptr(), g.data_ptr(), ptr(inv), ptr(det),
-        ptr(av), res.data_ptr(), ptr(bad), n_bl, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        ptr(av), res.data_ptr(), ptr(bad), n_bl, _stream_ptr(torch))
     _lib.check(rc, "txb_integrate_mesh")
     if bad is not None:
         i = int(bad.item())

@@ -118,16 +118,24 @@ def dump_mesh(mesh: Mesh, stream: TextIO) -> None:
 # device helpers
 # ---------------------------------------------------------------------------
 
+_CUDA_OK = False  # torch.cuda.is_available() seen True once
+
+
 def _torch():
+    global _CUDA_OK
     import torch
 
-    if not torch.cuda.is_available():
-        raise _lib.CudaLaneError("the CUDA lane needs a CUDA device (torch.cuda.is_available() is False)")
+    if not _CUDA_OK:
+        if not torch.cuda.is_available():
+            raise _lib.CudaLaneError("the CUDA lane needs a CUDA device (torch.cuda.is_available() is False)")
+        _CUDA_OK = True
     return torch
 
 
 def _stream_ptr(torch):
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    # current_stream(<int device>) skips torch's device-index resolution of the
+    # no-argument form (a few us per call on the mesh-level path)
+    return ctypes.c_void_p(torch.cuda.current_stream(torch.cuda.current_device()).cuda_stream)
 
 
 def _to_device(x, torch, dtype=None):

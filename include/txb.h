@@ -222,6 +222,16 @@ int txb_jit_integrate(void* kernel, int64_t n_cells, const void* basis, const vo
                       const void* weights, const void* inv_j, const void* det_j, const void* coeffs,
                       const void* aux, void* out, int n_bl, int n_cb, void* stream);
 
+/* The run-time compiled form on a mesh, fused like txb_integrate_mesh: device
+ * vertices (n_vertices, dim) float64, cells int64 (n_cells, dim+1),
+ * coeffs_global (n_vertices * n_comp) in the kernel's precision, per-cell aux
+ * as in txb_jit_integrate; the float64 geometry (cast once) and the gather
+ * run in-kernel; bad_cell as for txb_integrate_mesh.  Any tabulation. */
+int txb_jit_integrate_mesh(void* kernel, int64_t n_cells, int64_t n_vertices, const void* basis,
+                           const void* basis_der, const void* weights, const double* vertices,
+                           const int64_t* cells, const void* coeffs_global, const void* aux, void* out,
+                           int64_t* bad_cell, int n_bl, void* stream);
+
 /* ---- Halo exchange over peer memory (one node, NVLink / NVSwitch) --------
  * The global-residual exchange of halo.py without NCCL: every rank exposes a
  * WINDOW (header of epoch flags/acks + two receive slots of n_recv rows), shared

@@ -47,10 +47,23 @@ constexpr int S = (int)sizeof(real);
 // the banks (the cell-major odd stride left 4-way conflicts on the T loads).
 constexpr int P = CW + 4;
 constexpr int NF1 = NQ * NCOMP * D, NF0 = HAS_F0 ? NQ * NCOMP : 0;
-template <bool STD>
+// STAGE_T: only T[0] goes through the exchange area, the basis phase reads
+// the invJ rows from the stage (standard tables, cell-array entry points);
+// the mesh entry points compute invJ in-kernel and keep every T row there.
+template <bool STAGE_T>
 struct Area {
-  static constexpr int NTR = STD ? D : NQ * NB * D;  // rows of T in the exchange area
+  static constexpr int NTR = STAGE_T ? D : NQ * NB * D;  // rows of T in the exchange area
   static constexpr int BYTES = round_up(P * (NTR + NF1 + NF0) * S, 16);
+};
+
+// Mesh inputs of one batch: connectivity rows (stage or global), coordinates,
+// global coefficients, the orientation flag and the batch's first cell.
+struct MeshIn {
+  const int64_t* ids;
+  const double* X;
+  const real* glob;
+  unsigned long long* bad;
+  int64_t c0_batch;
 };
 
 __device__ __forceinline__ int inv_bytes(int n) { return round_up(n * DD * S, 16); }
@@ -58,13 +71,14 @@ __device__ __forceinline__ int det_bytes(int n) { return round_up(n * S, 16); }
 __device__ __forceinline__ int coef_bytes(int n) { return round_up(n * NBC * S, 16); }
 __device__ __forceinline__ int aux_bytes(int n) { return round_up(n * AUXW * S, 16); }
 
-template <bool STD, bool VEC>
+template <bool STD, bool VEC, bool MESH>
 __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const real* __restrict__ s_inv,
                                            const real* __restrict__ s_det, const real* __restrict__ s_coef,
                                            const real* __restrict__ s_aux, real* __restrict__ scratch, int c0,
-                                           int ncell, real* __restrict__ out, int lane) {
+                                           int ncell, real* __restrict__ out, int lane, const MeshIn& mi) {
+  constexpr bool STAGE_T = STD && !MESH;
   real* s_tr = scratch;
-  real* s_f1 = s_tr + P * Area<STD>::NTR;
+  real* s_f1 = s_tr + P * Area<STAGE_T>::NTR;
   real* s_f0 = s_f1 + P * NF1;
   const int nc = min(CW, ncell - c0);
 
@@ -74,10 +88,33 @@ __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const re
   if (lc < nc) {
     const int cell = c0 + lc;
     real J[DD];
-    load_row<real, DD, VEC>(s_inv + cell * DD, J);
     real cf[NBC];
-    load_row<real, NBC, VEC>(s_coef + cell * NBC, cf);
-    const real det = s_det[cell];
+    real det;
+    if constexpr (MESH) {
+      // gather (mesh.py:202-217) and float64 geometry (mesh.py:150-190), cast once to the run
+      // precision (executor.py:77-90): the reference's host steps, in-kernel
+      int64_t ids[NB];
+      load_row<int64_t, NB, VEC>(mi.ids + cell * NB, ids);
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int c = 0; c < NCOMP; ++c) cf[b * NCOMP + c] = __ldg(mi.glob + ids[b] * NCOMP + c);
+      double X[NB][D];
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int i = 0; i < D; ++i) X[b][i] = __ldg(mi.X + ids[b] * D + i);
+      double inv[DD], detd;
+      affine_inverse<D>(X, inv, detd);
+      if (q == 0 && mi.bad && detd <= 0.0) atomicMin(mi.bad, (unsigned long long)(mi.c0_batch + cell));
+#pragma unroll
+      for (int i = 0; i < DD; ++i) J[i] = (real)inv[i];
+      det = (real)detd;
+    } else {
+      load_row<real, DD, VEC>(s_inv + cell * DD, J);
+      load_row<real, NBC, VEC>(s_coef + cell * NBC, cf);
+      det = s_det[cell];
+    }
 
     // pulled-back gradients T[b][k] = sum_j D[q][b][j] invJ[j][k]  (_kernels_py.py:78-90)
     real tr[NB][D];
@@ -88,12 +125,18 @@ __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const re
 #pragma unroll
         for (int j = 1; j < D; ++j) acc = add(acc, -J[j * D + k]);
         tr[0][k] = acc;
-        if (q == 0) s_tr[k * P + lc] = acc;
+        if (STAGE_T && q == 0) s_tr[k * P + lc] = acc;
       }
 #pragma unroll
       for (int b = 1; b < NB; ++b)
 #pragma unroll
         for (int k = 0; k < D; ++k) tr[b][k] = J[(b - 1) * D + k];
+      if constexpr (!STAGE_T) {
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+          for (int k = 0; k < D; ++k) s_tr[((q * NB + b) * D + k) * P + lc] = tr[b][k];
+      }
     } else {
 #pragma unroll
       for (int b = 0; b < NB; ++b)
@@ -175,7 +218,7 @@ __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const re
     const int b = r / NCOMP;
     const int c = r - b * NCOMP;
     real e = real(0);  // _kernels_py.py:67-75: q-major, f0 term then the k terms
-    if constexpr (STD) {
+    if constexpr (STAGE_T) {
       // T[0] from the exchange area, T[b>=1] = invJ row b-1 (stage, or global on the direct path)
       real t[D];
       const real* tp = b == 0 ? s_tr + ec : s_inv + (c0 + ec) * DD + (b - 1) * D;
@@ -209,25 +252,35 @@ __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const re
   __syncwarp();  // scratch is reused by the next slice
 }
 
-template <bool STD>
-__device__ __forceinline__ void integrate_body(const IntegrateArgs<real>& a) {
-  constexpr int SCRATCH_BYTES = Area<STD>::BYTES;
+template <bool STD, bool MESH>
+__device__ __forceinline__ void integrate_body(const IntegrateArgs<real>& a, const MeshLaunchArgs<real>* m) {
+  constexpr int SCRATCH_BYTES = Area<STD && !MESH>::BYTES;
   extern __shared__ __align__(128) unsigned char smem[];
   const int nbc = a.n_bc;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int W = a.warps;
-  const int o_det = inv_bytes(nbc), o_coef = o_det + det_bytes(nbc), o_aux = o_coef + coef_bytes(nbc);
+  // stage: inv_j | det_j | coeffs | aux  (cell arrays)   or   cells (int64) | aux  (mesh)
+  const int o_det = MESH ? 0 : inv_bytes(nbc);
+  const int o_coef = MESH ? 0 : o_det + det_bytes(nbc);
+  const int o_aux = MESH ? round_up(nbc * NB * 8, 16) : o_coef + coef_bytes(nbc);
   const int stage_bytes = o_aux + aux_bytes(nbc);
   unsigned char* scratch_base = smem + a.stages * stage_bytes;
   const PipelineSmem p = carve_pipeline(scratch_base + W * SCRATCH_BYTES);
   pipeline_init(a, p);
   if (warp == W && lane == 0 && a.bulk) {
     pipeline_first_batches(a, a.prefetch, [&](int64_t c0, int ncell) {
-      const uint32_t ib = ncell * DD * S, db = ncell * S, cb = ncell * NBC * S, ab = ncell * AUXW * S;
-      if ((ib | db | cb | ab) & 15u) return;
-      bulk_prefetch_l2(a.inv_j + c0 * DD, ib);
-      bulk_prefetch_l2(a.det_j + c0, db);
-      bulk_prefetch_l2(a.coeffs + c0 * NBC, cb);
+      const uint32_t ab = ncell * AUXW * S;
+      if constexpr (MESH) {
+        const uint32_t kb = ncell * NB * 8;
+        if ((kb | ab) & 15u) return;
+        bulk_prefetch_l2(m->cells + c0 * NB, kb);
+      } else {
+        const uint32_t ib = ncell * DD * S, db = ncell * S, cb = ncell * NBC * S;
+        if ((ib | db | cb | ab) & 15u) return;
+        bulk_prefetch_l2(a.inv_j + c0 * DD, ib);
+        bulk_prefetch_l2(a.det_j + c0, db);
+        bulk_prefetch_l2(a.coeffs + c0 * NBC, cb);
+      }
       if (AUXW) bulk_prefetch_l2(a.aux + c0 * AUXW, ab);
     });
   }
@@ -238,12 +291,20 @@ __device__ __forceinline__ void integrate_body(const IntegrateArgs<real>& a) {
     if (lane != 0) return;
     const uint64_t policy = l2_evict_first_policy();
     pipeline_produce(a, p, smem, stage_bytes, [&](unsigned char* st, int64_t c0, int ncell, uint64_t* bar) {
-      const uint32_t ib = ncell * DD * S, db = ncell * S, cb = ncell * NBC * S, ab = ncell * AUXW * S;
-      if (!a.bulk || ((ib | db | cb | ab) & 15u)) return false;
-      mbar_arrive_expect_tx(bar, ib + db + cb + ab);
-      bulk_g2s(st, a.inv_j + c0 * DD, ib, bar, policy);
-      bulk_g2s(st + o_det, a.det_j + c0, db, bar, policy);
-      bulk_g2s(st + o_coef, a.coeffs + c0 * NBC, cb, bar, policy);
+      const uint32_t ab = ncell * AUXW * S;
+      if constexpr (MESH) {
+        const uint32_t kb = ncell * NB * 8;
+        if (!a.bulk || ((kb | ab) & 15u)) return false;
+        mbar_arrive_expect_tx(bar, kb + ab);
+        bulk_g2s(st, m->cells + c0 * NB, kb, bar, policy);
+      } else {
+        const uint32_t ib = ncell * DD * S, db = ncell * S, cb = ncell * NBC * S;
+        if (!a.bulk || ((ib | db | cb | ab) & 15u)) return false;
+        mbar_arrive_expect_tx(bar, ib + db + cb + ab);
+        bulk_g2s(st, a.inv_j + c0 * DD, ib, bar, policy);
+        bulk_g2s(st + o_det, a.det_j + c0, db, bar, policy);
+        bulk_g2s(st + o_coef, a.coeffs + c0 * NBC, cb, bar, policy);
+      }
       if (AUXW) bulk_g2s(st + o_aux, a.aux + c0 * AUXW, ab, bar, policy);
       return true;
     });
@@ -254,19 +315,26 @@ __device__ __forceinline__ void integrate_body(const IntegrateArgs<real>& a) {
   real* scratch = reinterpret_cast<real*>(scratch_base + warp * SCRATCH_BYTES);
   pipeline_consume(a, p, smem, stage_bytes, [&](const unsigned char* st, int64_t c0, int ncell) {
     real* out = a.out + c0 * NBC;
+    MeshIn mi{nullptr, nullptr, nullptr, nullptr, c0};
+    if constexpr (MESH) {
+      mi.ids = st ? reinterpret_cast<const int64_t*>(st) : m->cells + c0 * NB;
+      mi.X = m->vertices;
+      mi.glob = m->coeffs_global;
+      mi.bad = m->bad;
+    }
     if (st) {
       const real* s_inv = reinterpret_cast<const real*>(st);
       const real* s_det = reinterpret_cast<const real*>(st + o_det);
       const real* s_coef = reinterpret_cast<const real*>(st + o_coef);
       const real* s_aux = reinterpret_cast<const real*>(st + o_aux);
       for (int c = warp * CW; c < ncell; c += W * CW)
-        warp_slice<STD, true>(a.tab, s_inv, s_det, s_coef, s_aux, scratch, c, ncell, out, lane);
+        warp_slice<STD, true, MESH>(a.tab, s_inv, s_det, s_coef, s_aux, scratch, c, ncell, out, lane, mi);
     } else {
       // unaligned caller buffers or an odd-sized partial batch: straight from global memory
       const real* g_aux = AUXW ? a.aux + c0 * AUXW : nullptr;
       for (int c = warp * CW; c < ncell; c += W * CW)
-        warp_slice<STD, false>(a.tab, a.inv_j + c0 * DD, a.det_j + c0, a.coeffs + c0 * NBC, g_aux, scratch, c, ncell,
-                          out, lane);
+        warp_slice<STD, false, MESH>(a.tab, a.inv_j + c0 * DD, a.det_j + c0, a.coeffs + c0 * NBC, g_aux, scratch, c,
+                                     ncell, out, lane, mi);
     }
   });
 }
@@ -279,10 +347,22 @@ __device__ unsigned long long txb_jit_work_pool[4096][2];
 
 extern "C" __global__ void __launch_bounds__(txb::MAX_CTA_THREADS, 1)
 txb_jit_integrate(const __grid_constant__ txb::IntegrateArgs<real> a) {
-  txb::jit::integrate_body<false>(a);
+  txb::jit::integrate_body<false, false>(a, nullptr);
 }
 
 extern "C" __global__ void __launch_bounds__(txb::MAX_CTA_THREADS, 1)
 txb_jit_integrate_std(const __grid_constant__ txb::IntegrateArgs<real> a) {
-  txb::jit::integrate_body<true>(a);
+  txb::jit::integrate_body<true, false>(a, nullptr);
+}
+
+// mesh-fused: connectivity in, geometry + gather in-kernel (the reference's
+// compute_geometry -> gather_coefficients -> cast -> integrate, executor.py:194-212)
+extern "C" __global__ void __launch_bounds__(txb::MAX_CTA_THREADS, 1)
+txb_jit_integrate_mesh(const __grid_constant__ txb::MeshLaunchArgs<real> m) {
+  txb::jit::integrate_body<false, true>(m.a, &m);
+}
+
+extern "C" __global__ void __launch_bounds__(txb::MAX_CTA_THREADS, 1)
+txb_jit_integrate_mesh_std(const __grid_constant__ txb::MeshLaunchArgs<real> m) {
+  txb::jit::integrate_body<true, true>(m.a, &m);
 }

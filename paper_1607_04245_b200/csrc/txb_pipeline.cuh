@@ -52,6 +52,18 @@ struct IntegrateArgs {
   Tabulation<T> tab;
 };
 
+// Arguments of a mesh-fused kernel: the batch pipeline's (cells, batches,
+// tables, aux, out) plus the mesh -- connectivity (streamed through the
+// stage), vertex coordinates and the global coefficient vector (gathered).
+template <typename T>
+struct MeshLaunchArgs {
+  IntegrateArgs<T> a;           // inv_j / det_j / coeffs unused
+  const int64_t* cells;         // (n_cells, D+1)
+  const double* vertices;       // (n_vertices, D)
+  const T* coeffs_global;       // (n_vertices * n_comp), run precision
+  unsigned long long* bad;      // lowered to the first cell with detJ <= 0 (NULL = no check)
+};
+
 // 16- and 8-byte vector types per element type (type-preserving: the lanes of
 // the vector ARE elements of the row, no conversion).
 template <typename T> struct Vec16;

@@ -21,6 +21,7 @@ Differences from the reference, all deliberate:
 
 from __future__ import annotations
 
+import os
 from dataclasses import replace
 from typing import Optional, Union
 
@@ -234,6 +235,9 @@ def integrate_transposed(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule:
         # geometry + gather + cast + integrate in one kernel (csrc/txb_integrate_mesh.cu)
         elem = integrate_mesh(mesh, layout, tab, rule, form, glob_dev, aux_dev, dtype=dt, cell_geom=cell_geom,
                               cells=cells_dev, vertices=verts_dev, n_bl=n_bl)
+    elif isinstance(kernel, _backend.JitKernel) and cell_geom is None and os.environ.get("TXB_JIT_MESH", "1") != "0":
+        # run-time compiled form, fused the same way (csrc/txb_jit_kernel.cuh, mesh entry points)
+        elem = _jit_mesh(kernel, mesh, tab, rule, form, glob_dev, aux_dev, dt, cells_dev, verts_dev, n_bl)
     else:
         if cell_geom is None:
             cell_geom = compute_geometry(mesh, cells=cells_dev, vertices=verts_dev, device_out=True)
@@ -253,6 +257,35 @@ def integrate_transposed(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule:
 
 
 _FUSABLE: dict = {}
+
+
+def _jit_mesh(kernel, mesh: Mesh, tab: Tabulation, rule: QuadratureRule, form: PhysicsForm, glob_dev, aux_dev, dt,
+              cells_dev, verts_dev, n_bl: int):
+    """Element vectors of a run-time compiled form straight from the mesh
+    (txb_jit_integrate_mesh: float64 geometry + gather in-kernel, any
+    tabulation).  Raises OrientationError for a cell with detJ <= 0."""
+    import ctypes
+
+    from . import _lib
+    from .errors import OrientationError
+
+    torch = _torch()
+    n = mesh.n_cells
+    if int(glob_dev.numel()) != mesh.n_vertices * form.n_comp:
+        raise ShapeError(f"global vector has {glob_dev.numel()} entries, expected {mesh.n_vertices * form.n_comp}")
+    res = torch.empty((n, tab.n_b, form.n_comp), dtype=glob_dev.dtype, device="cuda")
+    bad = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    B, D, W = (np.ascontiguousarray(x, dtype=dt) for x in (tab.basis, tab.basis_der, rule.weights))
+    av = None if aux_dev is None else aux_dev.values.contiguous()
+    rc = _lib.lib().txb_jit_integrate_mesh(ctypes.c_void_p(kernel.handle), n, mesh.n_vertices, B.ctypes.data,
+                                           D.ctypes.data, W.ctypes.data, verts_dev.data_ptr(), cells_dev.data_ptr(),
+                                           glob_dev.data_ptr(), None if av is None else av.data_ptr(),
+                                           res.data_ptr(), bad.data_ptr(), n_bl, _stream_ptr(torch))
+    _lib.check(rc, "txb_jit_integrate_mesh")
+    i = int(bad.item())
+    if i >= 0:
+        raise OrientationError(f"cell {i} is degenerate or negatively oriented")
+    return res
 
 
 def _mesh_fusable(tab: Tabulation, rule: QuadratureRule) -> bool:

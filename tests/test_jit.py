@@ -59,7 +59,14 @@ def test_jit_cubin_is_sm100a_bulk_copy_pipeline(tmp_path):
     assert "sm_100a" in sass
     assert "UBLKCP" in sass  # cp.async.bulk global -> shared (the batch loader)
     assert "SYNCS" in sass   # mbarrier ring
-    assert "DFMA" not in sass  # -fmad=false: every product and sum rounds on its own
+    funcs = {}
+    for part in sass.split("Function : ")[1:]:
+        funcs[part.split()[0]] = part
+    assert {"txb_jit_integrate", "txb_jit_integrate_std", "txb_jit_integrate_mesh",
+            "txb_jit_integrate_mesh_std"} <= set(funcs)
+    # -fmad=false: every product and sum rounds on its own.  The only FMAs are the mesh
+    # entry points' explicit correction steps of the correctly rounded x / detJ (DetDivider).
+    assert "DFMA" not in funcs["txb_jit_integrate"] and "DFMA" not in funcs["txb_jit_integrate_std"]
     res = subprocess.run(["cuobjdump", "-res-usage", str(p)], capture_output=True, text=True, check=True).stdout
     assert "LOCAL:0" in res  # no spills
 
@@ -246,6 +253,44 @@ def test_jit_standard_table_entry_point_matches_generic(name, dim, monkeypatch):
             gen = _run(k, tab.basis, tab.basis_der, rule.weights, inv, det, co, aux, dt)
             assert bitwise_equal(std, want), (rule.n_q, dt)
             assert bitwise_equal(gen, want), (rule.n_q, dt)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", SPECS)
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_integrate_transposed_user_forms_mesh_fused(name, dim, dtype):
+    """integrate_transposed with a run-time compiled form: the mesh entry point
+    (float64 geometry + gather in-kernel, txb_jit_integrate_mesh) on a perturbed
+    Kuhn mesh with a shuffled vertex numbering, midpoint and two-point rules,
+    then the scatter-add — bit-identical to the oracle's geometry -> gather ->
+    python-lane integration -> np.add.at, and to the unfused route (given
+    geometry: gather + txb_jit_integrate)."""
+    s = user_forms.spec(name, dim)
+    f = form_of(name, dim)
+    npdt = np.float64 if dtype == "f64" else np.float32
+    base = txb.generate_unit_simplex_mesh(dim, 11 if dim == 2 else 4)
+    rng = np.random.default_rng(dim * 7 + len(name))
+    perm = rng.permutation(base.n_vertices)
+    verts = base.vertices[np.argsort(perm)] + 0.02 * rng.uniform(-1, 1, base.vertices.shape)
+    mesh = txb.Mesh(dim, np.ascontiguousarray(verts), np.ascontiguousarray(perm[base.cells]))
+    layout = txb.FieldLayout(s["n_comp"])
+    glob = rng.standard_normal(layout.global_size(mesh))
+    aux = aux_for(s, mesh.n_cells, rng)
+    inv, det = oracle.geometry(mesh.vertices, mesh.cells)
+    for rule in (txb.quadrature_rule(dim, 1), txb.two_point_rule(dim)):
+        tab = txb.tabulate(dim, rule)
+        res, _ = txb.integrate_transposed(mesh, layout, tab, rule, f, glob, aux, n_bl=8, n_cb=2, dtype=dtype,
+                                          shared_mem_limit=None)
+        elem = oracle.integrate_forms(s["f1_many"], s["f0_many"], s["uses_grad_a"], s["aux"], tab.basis,
+                                      tab.basis_der, rule.weights, inv, det,
+                                      oracle.gather(mesh.cells, glob, s["n_comp"]),
+                                      None if aux is None else aux.values, npdt)
+        want = oracle.scatter_add(mesh.cells, elem, mesh.n_vertices)
+        assert bitwise_equal(res, want), (rule.n_q, dtype)
+        res2, _ = txb.integrate_transposed(mesh, layout, tab, rule, f, glob, aux, n_bl=8, n_cb=2, dtype=dtype,
+                                           shared_mem_limit=None, cell_geom=txb.CellGeometry(inv, det))
+        assert bitwise_equal(res2, want)
 
 
 @pytest.mark.gpu

@@ -6,7 +6,8 @@
 Covers the ahead-of-time integration kernel (all forms, f32/f64, n_q 1-3,
 static and dynamic batch scheduling, ragged tails, unaligned buffers), the
 fused mesh kernel (given and in-kernel geometry), gather, incidence build,
-scatter-add, geometry, the run-time compiled kernel and the halo pack/assemble.
+scatter-add, geometry, the run-time compiled kernel (cell arrays and mesh entry
+points) and the halo pack/assemble.
 Every result is checked against the oracle so a sanitizer run is also a
 parity run.  Test/tuning infrastructure: uses oracle/ as the checker.
 """
@@ -124,6 +125,25 @@ def main():
         ref = oracle.integrate_forms(s["f1_many"], s["f0_many"], s["uses_grad_a"], s["aux"], B, D, W, inv, det, co,
                                      None if aux is None else aux.values)
         assert out.cpu().numpy().tobytes() == ref.tobytes(), name
+        checks += 1
+        # the same form on a mesh: the mesh entry point (geometry + gather in-kernel) + scatter-add
+        mesh = txb.generate_unit_simplex_mesh(3, 3)
+        layout = txb.FieldLayout(s["n_comp"])
+        glob = rng.standard_normal(layout.global_size(mesh))
+        maux = None
+        if s["aux"]:
+            shape = (mesh.n_cells, s["n_aux"]) if s["aux"] == "p0" else (mesh.n_cells, 4, s["n_aux"])
+            maux = CellAux(s["aux"], rng.uniform(0.5, 1.5, shape))
+        rule = txb.quadrature_rule(3, 1)
+        tab = txb.tabulate(3, rule)
+        res, _ = txb.integrate_transposed(mesh, layout, tab, rule, f, glob, maux, n_bl=8, n_cb=2,
+                                          shared_mem_limit=None)
+        minv, mdet = oracle.geometry(mesh.vertices, mesh.cells)
+        elem = oracle.integrate_forms(s["f1_many"], s["f0_many"], s["uses_grad_a"], s["aux"], tab.basis,
+                                      tab.basis_der, rule.weights, minv, mdet,
+                                      oracle.gather(mesh.cells, glob, s["n_comp"]),
+                                      None if maux is None else maux.values)
+        assert res.tobytes() == oracle.scatter_add(mesh.cells, elem, mesh.n_vertices).tobytes(), name
         checks += 1
     print(f"sanitize_workload: {checks} checks bit-identical to the oracle", flush=True)
 

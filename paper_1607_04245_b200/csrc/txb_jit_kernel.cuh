@@ -345,6 +345,7 @@ __device__ __forceinline__ void integrate_body(const IntegrateArgs<real>& a, con
 // dynamic-scheduling counters of this module (zero at load, self-resetting)
 __device__ unsigned long long txb_jit_work_pool[4096][2];
 
+#ifndef TXB_JIT_MESH
 extern "C" __global__ void __launch_bounds__(txb::MAX_CTA_THREADS, 1)
 txb_jit_integrate(const __grid_constant__ txb::IntegrateArgs<real> a) {
   txb::jit::integrate_body<false, false>(a, nullptr);
@@ -355,8 +356,10 @@ txb_jit_integrate_std(const __grid_constant__ txb::IntegrateArgs<real> a) {
   txb::jit::integrate_body<true, false>(a, nullptr);
 }
 
+#else
 // mesh-fused: connectivity in, geometry + gather in-kernel (the reference's
-// compute_geometry -> gather_coefficients -> cast -> integrate, executor.py:194-212)
+// compute_geometry -> gather_coefficients -> cast -> integrate, executor.py:194-212).
+// A second program (TXB_JIT_MESH), compiled on first use by txb_jit_integrate_mesh.
 extern "C" __global__ void __launch_bounds__(txb::MAX_CTA_THREADS, 1)
 txb_jit_integrate_mesh(const __grid_constant__ txb::MeshLaunchArgs<real> m) {
   txb::jit::integrate_body<false, true>(m.a, &m);
@@ -366,3 +369,4 @@ extern "C" __global__ void __launch_bounds__(txb::MAX_CTA_THREADS, 1)
 txb_jit_integrate_mesh_std(const __grid_constant__ txb::MeshLaunchArgs<real> m) {
   txb::jit::integrate_body<true, true>(m.a, &m);
 }
+#endif

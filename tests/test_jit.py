@@ -62,10 +62,8 @@ def test_jit_cubin_is_sm100a_bulk_copy_pipeline(tmp_path):
     funcs = {}
     for part in sass.split("Function : ")[1:]:
         funcs[part.split()[0]] = part
-    assert {"txb_jit_integrate", "txb_jit_integrate_std", "txb_jit_integrate_mesh",
-            "txb_jit_integrate_mesh_std"} <= set(funcs)
-    # -fmad=false: every product and sum rounds on its own.  The only FMAs are the mesh
-    # entry points' explicit correction steps of the correctly rounded x / detJ (DetDivider).
+    assert {"txb_jit_integrate", "txb_jit_integrate_std"} <= set(funcs)  # mesh entry points: own program
+    # -fmad=false: every product and sum rounds on its own
     assert "DFMA" not in funcs["txb_jit_integrate"] and "DFMA" not in funcs["txb_jit_integrate_std"]
     res = subprocess.run(["cuobjdump", "-res-usage", str(p)], capture_output=True, text=True, check=True).stdout
     assert "LOCAL:0" in res  # no spills

@@ -415,6 +415,32 @@ def api_rows(steps=20):
         del glob_dev, aux_dev
         del geom
         torch.cuda.empty_cache()
+    # a run-time compiled user form (f0, two P1 fields, grad a) at mesh level, device-resident:
+    # the mesh entry point of the NVRTC lane (geometry + gather in-kernel) + scatter-add
+    from paper_1607_04245_b200.physics import user_form
+
+    dim, _, dtype, n = CONFIGS["3d_varcoef_f64"]
+    mesh = txb.generate_unit_simplex_mesh(dim, refine_for(dim, n))
+    form = user_form("advect", 3, 1, lambda s, c: None, 9, ADVECT_F1, n_aux=2, f0=lambda s, c: None,
+                     flops_f0=7, source_f0=ADVECT_F0, uses_grad_a=True)
+    layout = txb.FieldLayout(1)
+    rule = txb.quadrature_rule(dim, 1)
+    tab = txb.tabulate(dim, rule)
+    glob_dev = torch.from_numpy(np.random.default_rng(5).standard_normal(mesh.n_vertices)).cuda()
+    aux_dev = txb.CellAux("p1", torch.rand((mesh.n_cells, dim + 1, 2), dtype=torch.float64, device="cuda") + 0.5)
+    call = lambda: txb.integrate_transposed(mesh, layout, tab, rule, form, glob_dev, aux_dev, n_bl=32,  # noqa: E731
+                                            n_cb=8, dtype=dtype, shared_mem_limit=None)
+    for _ in range(3):
+        call()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        call()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / steps
+    rows.append({"config": "api_integrate_transposed_device_user_advect_3d_f64", "cells": mesh.n_cells,
+                 "vertices": mesh.n_vertices, "ms_per_call": dt * 1e3, "gcells_per_s": mesh.n_cells / dt / 1e9,
+                 "path": "CUDA tensors in/out: run-time compiled form, mesh entry point + scatter-add"})
     return rows
 
 

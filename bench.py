@@ -147,40 +147,63 @@ def dist_setup():
     return world, rank, local
 
 
-def rank_workload(name, rank, world, seed=1234):
-    """Rank r's contiguous cell range of the N x cells-per-GPU Kuhn mesh, generated on its GPU."""
-    import torch
-
-    from paper_1607_04245_b200.mesh import CellGeometry, FieldLayout, Mesh, compute_geometry, \
-        gather_coefficients, generate_unit_simplex_mesh
-    from paper_1607_04245_b200.physics import CellAux
+def rank_plan(name, rank, world):
+    """(lo, hi, refinement) of rank r's contiguous cell range of the
+    world x cells-per-GPU job (shard.cell_range, 256-cell aligned)."""
     from paper_1607_04245_b200.shard import cell_range
-    from paper_1607_04245_b200.workload import PHYSICS, refine_for
-    from paper_1607_04245_b200.element import quadrature_rule, tabulate
+    from paper_1607_04245_b200.workload import refine_for
 
-    dim, physics, dtype, per_gpu = CONFIGS[name]
+    dim, _, _, per_gpu = CONFIGS[name]
     total = per_gpu * world
     lo, hi = cell_range(total, rank, world, align=256)
+    return lo, hi, refine_for(dim, total)
+
+
+def rank_host_inputs(name, rank, world, seed=1234):
+    """Host side of rank r's workload: its cells of the Kuhn mesh holding
+    world x per-GPU cells (only rows [lo, hi) are generated), the mesh's vertex
+    coordinates, the global N(0,1) coefficient vector and the rank's slice of
+    the P0 kappa field (PCG64 jumped ahead to lo).  Identical to slicing the
+    full single-process workload (tests/test_distributed.py)."""
+    from paper_1607_04245_b200.workload import PHYSICS, kuhn_cells, kuhn_vertices, uniform_slice
+
+    dim, physics, _, _ = CONFIGS[name]
+    lo, hi, r = rank_plan(name, rank, world)
     factory, aux_space = PHYSICS[physics]
     form = factory(dim)
+    verts = kuhn_vertices(dim, r)
+    cells = kuhn_cells(dim, r, lo, hi)
+    glob = np.random.default_rng(seed).standard_normal(verts.shape[0] * form.n_comp)
+    kappa = uniform_slice(seed + 1, lo, hi) if aux_space == "p0" else None
+    return dict(form=form, lo=lo, hi=hi, vertices=verts, cells=cells, glob=glob, kappa=kappa)
+
+
+def rank_workload(name, rank, world, seed=1234):
+    """Rank r's contiguous cell range of the N x cells-per-GPU Kuhn mesh: host
+    generation of its rows only, geometry and gather on its GPU."""
+    import torch
+
+    from paper_1607_04245_b200.element import quadrature_rule, tabulate
+    from paper_1607_04245_b200.mesh import FieldLayout, Mesh, compute_geometry, gather_coefficients
+    from paper_1607_04245_b200.physics import CellAux
+
+    dim, physics, dtype, per_gpu = CONFIGS[name]
+    h = rank_host_inputs(name, rank, world, seed)
+    form = h["form"]
     rule = quadrature_rule(dim, 1)
     tab = tabulate(dim, rule)
-    full = generate_unit_simplex_mesh(dim, refine_for(dim, total))
-    cells_np = np.ascontiguousarray(full.cells[lo:hi])
-    cells = torch.from_numpy(cells_np).to("cuda")
-    sliced = Mesh(dim, full.vertices, cells_np)
+    cells = torch.from_numpy(h["cells"]).to("cuda")
+    sliced = Mesh(dim, h["vertices"], h["cells"])
     geom = compute_geometry(sliced, cells=cells, device_out=True)
     layout = FieldLayout(form.n_comp)
-    glob = np.random.default_rng(seed).standard_normal(layout.global_size(full))
-    coeffs = gather_coefficients(sliced, layout, torch.from_numpy(glob).to("cuda"), cells=cells)
+    coeffs = gather_coefficients(sliced, layout, torch.from_numpy(h["glob"]).to("cuda"), cells=cells)
     tdt = torch.float32 if dtype == "f32" else torch.float64
     aux = None
-    if aux_space == "p0":
-        vals = np.random.default_rng(seed + 1).uniform(0.5, 1.5, (full.n_cells, 1))[lo:hi]
-        aux = CellAux("p0", torch.from_numpy(np.ascontiguousarray(vals)).to("cuda", tdt))
+    if h["kappa"] is not None:
+        aux = CellAux("p0", torch.from_numpy(np.ascontiguousarray(h["kappa"])).to("cuda", tdt))
     c = lambda t: t.to(tdt).contiguous()  # noqa: E731
     return dict(form=form, rule=rule, tab=tab, inv=c(geom.inv_jacobians), det=c(geom.determinants),
-                coeffs=c(coeffs), aux=aux, n=hi - lo, dtype=dtype, dim=dim)
+                coeffs=c(coeffs), aux=aux, n=h["hi"] - h["lo"], dtype=dtype, dim=dim)
 
 
 def time_device(wl, steps, warmup, n_sets, barrier=None, sampler=None, jit=False):
@@ -208,7 +231,9 @@ def time_device(wl, steps, warmup, n_sets, barrier=None, sampler=None, jit=False
         inv, det, co, aux, out = sets[i % n_sets]
         backend.run_cuda(kernel, B, D, W, inv, det, co, aux, out)
 
-    for i in range(warmup):
+    # warm-up writes EVERY set's output at least once (the determinism check
+    # below compares all of them, whatever K and W are)
+    for i in range(warmup_launches(warmup, n_sets)):
         launch(i)
     torch.cuda.synchronize()
     graph, mode = None, "graph"
@@ -249,9 +274,21 @@ def time_device(wl, steps, warmup, n_sets, barrier=None, sampler=None, jit=False
     total = t0.elapsed_time(t1)
     # every set holds identical inputs, so identical outputs: a cheap race/determinism check
     for k in range(1, n_sets):
-        assert torch.equal(sets[0][4], sets[k][4])
+        if not torch.equal(sets[0][4], sets[k][4]):
+            raise RuntimeError(f"buffer set {k} differs from set 0 after identical launches")
     del graph
     return total, mode
+
+
+def warmup_launches(warmup: int, n_sets: int) -> int:
+    """Untimed launches before capture: at least W, and at least one per buffer set."""
+    return max(warmup, n_sets)
+
+
+def rotating_sets(set_bytes: int, min_sets: int = 4, cap: int = 64) -> int:
+    """Buffer sets so that (sets - 1) x set bytes > 3 x L2: a step's inputs were
+    evicted by the steps in between (L2 flushed by the rotation)."""
+    return max(min_sets, min(cap, -(-3 * L2_BYTES // max(1, set_bytes)) + 1))
 
 
 def time_mesh(name, steps, warmup, n_sets_min=4, given_geometry=False):
@@ -673,14 +710,83 @@ class _NoBarrier:
 
 
 # ----------------------------------------------------------------------------
+def _guarded(rows, label, fn, *args, **kw):
+    """Run one extra row group; an exception becomes an {"error"} row instead of
+    discarding the headline line (which is assembled before any extra)."""
+    import traceback
+
+    try:
+        rows.extend(fn(*args, **kw))
+    except Exception as e:  # noqa: BLE001 - recorded in the JSON line
+        rows.append({"config": label, "error": f"{type(e).__name__}: {e}",
+                     "where": traceback.format_exc(limit=3).splitlines()[-3:]})
+    finally:
+        try:
+            import torch
+
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def variant_rows(peak, steps):
+    """The other BASELINE.json configurations on one GPU (parity configs timed
+    like the headline: device-resident, rotating buffer sets > 3x L2)."""
+    rows = []
+    for v in VARIANTS:
+        def one(v=v):
+            vf, vb = config_model(v)
+            vw = rank_workload(v, 0, 1)
+            ns = rotating_sets(vb * vw["n"])
+            k = variant_steps(vw["n"], steps)
+            tot, _ = time_device(vw, k, 5, ns)
+            vl = tot / k
+            return [{"config": v, "dtype": vw["dtype"], "cells": vw["n"], "steps": k, "sets": ns,
+                     "gflops": vf * vw["n"] / (vl * 1e-3) / 1e9,
+                     "gbs_launch": vb * vw["n"] / (vl * 1e-3) / 1e9,
+                     "frac": vb * vw["n"] / (vl * 1e-3) / 1e9 / peak, "launch_ms": vl,
+                     "bytes_per_cell": vb}]
+        _guarded(rows, v, one)
+    return rows
+
+
+def variant_steps(n_cells: int, steps: int) -> int:
+    """Launches timed per variant: >= 50 (so a short driver run still averages
+    over many launches), a quarter of K for long runs, capped at 1000."""
+    return min(1000, max(50, steps // 4)) if n_cells <= (1 << 20) else 40
+
+
+def mesh_rows(peak, steps):
+    rows = []
+    for v in ("3d_varcoef_f64", "3d_varcoef_f32", "3d_elasticity_f64", "2d_varcoef_f64"):
+        for given in (True, False):
+            def one(v=v, given=given):
+                vf, _ = config_model(v)
+                n = CONFIGS[v][3]
+                ms, per_cell = time_mesh(v, variant_steps(n, steps), 5, given_geometry=given)
+                return [{
+                    "config": ("mesh_given_geometry_" if given else "mesh_geometry_in_kernel_") + v,
+                    "path": "txb_integrate_mesh: gather" + ("" if given else " + float64 geometry") +
+                            " fused into the integration (replaces gather kernel + integrate_cells)",
+                    "cells": n, "launch_ms": ms, "gflops": vf * n / (ms * 1e-3) / 1e9,
+                    "gcells_per_s": n / (ms * 1e-3) / 1e9, "bytes_per_cell": per_cell,
+                    "gbs": per_cell * n / (ms * 1e-3) / 1e9, "frac": per_cell * n / (ms * 1e-3) / 1e9 / peak}]
+            _guarded(rows, f"mesh_{v}_{'given' if given else 'in_kernel'}", one)
+    return rows
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=4000)
+    ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=HEADLINE, choices=sorted(CONFIGS))
-    ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="headline only (no BASELINE variant rows)")
+    ap.add_argument("--extras", action="store_true",
+                    help="also the mesh-fused rows, the 2^24..2^27 sweep, the mesh-level API rows and the "
+                         "run-time compiled rows (minutes; not part of the default driver run)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=3.0)
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (profiling runs)")
@@ -694,12 +800,13 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        r = cpu_reference(args.config, args.steps + args.warmup, total_cells=per_gpu * max(world, args.gpus))
+        r = cpu_reference(args.config, args.steps + args.warmup, total_cells=per_gpu * max(world, args.gpus),
+                          target_s=None if args.steps + args.warmup <= 200 else 60.0)
         ts = r["times"][args.warmup:] if len(r["times"]) > args.warmup else r["times"]
         t = sum(ts) / len(ts)
         gf = flops_cell * r["n"] / t / 1e9
         line = {
-            "impl": "reference", "metric": "element-integration GF/s (paper Eq.7 flops)", "value": gf,
+            "impl": "reference", "metric": METRIC, "value": gf,
             "unit": "GF/s", "n_gpus": args.gpus, "steps": len(ts), "warmup": args.warmup,
             "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": dtype, "data": "synthetic (Kuhn mesh, seeded N(0,1) coefficients, P0 kappa)",
@@ -722,6 +829,7 @@ def main():
     device = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(device)
     barrier = None
+    dist = None
     if world > 1:
         import torch.distributed as dist
 
@@ -733,27 +841,25 @@ def main():
 
     def reduce_max(x: float) -> float:
         """max over ranks (timing of a multi-GPU step is the slowest rank)."""
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda" if dist_backend == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t[0])
+        return reduce_max_over_ranks(x, world, dist, "cuda" if dist_backend == "nccl" else "cpu")
 
     from paper_1607_04245_b200 import backend
 
+    # ------------------------------------------------------------------ headline
     wl = rank_workload(args.config, rank, world)
     set_bytes = bytes_cell * wl["n"]
-    n_sets = max(4, -(-3 * L2_BYTES // set_bytes) + 1)
+    n_sets = rotating_sets(set_bytes)
     sampler = ClockSampler(torch.cuda.current_device())
     total_ms, timing_mode = time_device(wl, args.steps, args.warmup, n_sets, barrier, sampler)
     total_ms = reduce_max(total_ms)
-    launch_ms = total_ms / args.steps  # one kernel launch per step
-    cells_total = per_gpu * world
-    ms_step = total_ms / args.steps
+    cells_total = sum(cell_counts(per_gpu, world))
+    ms_step = total_ms / args.steps  # one kernel launch per step
     gf = flops_cell * cells_total / (ms_step * 1e-3) / 1e9
+    # the roofline's launch time is THIS rank's own (rank 0 prints it)
+    launch_ms_local = ms_step
 
     # e2e through the host-buffer C ABI path
-    e2e_steps = max(3, min(20, args.steps // 20))
+    e2e_steps = max(3, min(20, args.steps))
     if barrier:
         barrier()
     if args.no_e2e:
@@ -763,93 +869,121 @@ def main():
         e2e_s = reduce_max(e2e_s)
         e2e_gf = flops_cell * cells_total * e2e_steps / e2e_s / 1e9
 
-    strong = strong_scaling_rows(world, rank, barrier, reduce_max) if world > 1 else None
-
-    if rank != 0:
+    line = None
+    if rank == 0:
+        peak, peak_src = peaks()
+        achieved = bytes_cell * wl["n"] / (launch_ms_local * 1e-3) / 1e9
+        form = wl["form"]
+        cfg = backend.launch_config(*backend.cuda_kernel(form, 1, wl["aux"], 4 if dtype == "f32" else 8),
+                                    4 if dtype == "f32" else 8, dim, 1, form.n_comp, wl["n"])
+        try:
+            achievable = stream_probe(wl["inv"].nbytes + wl["det"].nbytes + wl["coeffs"].nbytes +
+                                      (wl["aux"].values.nbytes if wl["aux"] is not None else 0),
+                                      wl["coeffs"].nbytes)
+        except Exception:  # noqa: BLE001 - optional context number
+            achievable = None
+        line = {
+            "metric": METRIC,
+            "value": gf, "unit": "GF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": dtype, "data": "synthetic (Kuhn mesh cells of the rank's range, seeded N(0,1) "
+                                    "coefficients, P0 kappa U[0.5,1.5); generated per rank)",
+            "config": {"workload": f"{args.config}: {dim}D P1 {physics}, {per_gpu} cells per GPU "
+                                   f"(BASELINE.json configs[1])",
+                       "cells_total": cells_total, "parallelism": f"cell-range x{world}",
+                       "l2": f"inputs > L2: {n_sets} rotating buffer sets of {set_bytes / 1e6:.1f} MB "
+                             f"(> 3 x 126 MB L2 between reuses)",
+                       "launch": cfg},
+            "gbs": bytes_cell * cells_total / (ms_step * 1e-3) / 1e9,
+            "cells_per_s": cells_total / (ms_step * 1e-3),
+            "roofline": roofline_entry(args.config, achieved, peak, peak_src, bytes_cell, flops_cell,
+                                       achievable, launch_ms_local, timing_mode, args.steps, wl["n"]),
+            "e2e": {"value": e2e_gf, "unit": "GF/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "steps": e2e_steps, "path": "txb_integrate_cells_host (pinned numpy in/out)"},
+            "gpu_launches": args.steps,
+            "clocks": sampler.summary(),
+        }
+        if world == 1 and not args.no_cpu:
+            try:
+                r = cpu_reference(args.config, 3, target_s=args.cpu_seconds)
+                t = statistics.median(r["times"])
+                line["cpu_baseline"] = {
+                    "value": flops_cell * r["n"] / t / 1e9, "unit": "GF/s", "cores": r["cores"],
+                    "kind": r["kind"], "ms": t * 1e3,
+                    "sample": f"{r['n']} cells ({args.config}) x {len(r['times'])} passes, fork pool of "
+                              f"{r['cores']} processes, median pass"}
+            except Exception as e:  # noqa: BLE001
+                line["cpu_baseline"] = {"value": None, "error": f"{type(e).__name__}: {e}"}
+    try:
+        # -------------------------------------------------------------- extras
+        # (each row group guarded: a failure is an error row, never a lost headline)
+        if world == 1 and rank == 0:
+            rows = []
+            peak = line["roofline"]["peak"]
+            if not args.no_variants:
+                rows += variant_rows(peak, args.steps)
+            if args.extras:
+                rows += mesh_rows(peak, args.steps)
+                _guarded(rows, "sweep", sweep_rows, peak)
+                _guarded(rows, "api", api_rows)
+                _guarded(rows, "jit", jit_rows, peak, variant_steps(1 << 20, args.steps))
+            if rows:
+                line["variants"] = rows
+        if world > 1:
+            try:
+                strong = strong_scaling_rows(world, rank, barrier, reduce_max)
+            except Exception as e:  # noqa: BLE001
+                strong = [{"error": f"{type(e).__name__}: {e}"}]
+            if line is not None:
+                line["strong_scaling"] = strong
+    finally:
+        if line is not None:
+            print(json.dumps(line), flush=True)
         if world > 1:
             dist.destroy_process_group()
-        return
 
-    peak, peak_src = peaks()
-    achieved = bytes_cell * wl["n"] / (launch_ms * 1e-3) / 1e9
-    form = wl["form"]
-    cfg = backend.launch_config(*backend.cuda_kernel(form, 1, wl["aux"], 4 if dtype == "f32" else 8),
-                                4 if dtype == "f32" else 8, dim, 1, form.n_comp, wl["n"])
-    achievable = stream_probe(wl["inv"].nbytes + wl["det"].nbytes + wl["coeffs"].nbytes +
-                              (wl["aux"].values.nbytes if wl["aux"] is not None else 0), wl["coeffs"].nbytes)
+
+def cell_counts(per_gpu: int, world: int):
+    """Cells of each rank's contiguous range of the world x per_gpu-cell job."""
+    from paper_1607_04245_b200.shard import cell_range
+
+    total = per_gpu * world
+    return [hi - lo for lo, hi in (cell_range(total, r, world, align=256) for r in range(world))]
+
+
+def reduce_max_over_ranks(x: float, world: int, dist, device: str) -> float:
+    """max over ranks of a float (time of a multi-GPU step = the slowest rank)."""
+    if world == 1:
+        return x
+    import torch
+
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t[0])
+
+
+def roofline_entry(config, achieved, peak, peak_src, bytes_cell, flops_cell, achievable, launch_ms, mode, steps,
+                   n_cells):
+    """The roofline object of the JSON line.  ``traffic`` is the ncu-measured
+    DRAM read + write bytes of ONE launch (write-back included), per cell, from
+    profiles/ncu_traffic.json (tools/traffic.py), scaled to this launch's cells."""
     prof = REPO / "profiles" / "ncu_traffic.json"
-    traffic = None
+    traffic = traffic_split = None
     if prof.exists():
-        traffic = json.loads(prof.read_text()).get(args.config)
-    line = {
-        "metric": "element-integration GF/s (paper Eq.7 flops)",
-        "value": gf, "unit": "GF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": dtype, "data": "synthetic (Kuhn mesh sliced to the cell count, seeded N(0,1) "
-                                "coefficients, P0 kappa U[0.5,1.5); generated on the device)",
-        "config": {"workload": f"{args.config}: {dim}D P1 {physics}, {per_gpu} cells per GPU "
-                               f"(BASELINE.json configs[1])",
-                   "cells_total": cells_total, "parallelism": f"cell-range x{world}",
-                   "l2": f"{n_sets} rotating buffer sets of {set_bytes / 1e6:.1f} MB (> 126 MB L2)",
-                   "launch": cfg},
-        "gbs": bytes_cell * cells_total / (ms_step * 1e-3) / 1e9,
-        "cells_per_s": cells_total / (ms_step * 1e-3),
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "bytes_per_cell": bytes_cell, "flops_per_cell_eq7": flops_cell,
-                     "achievable_stream_gbs": achievable, "frac_of_achievable": achieved / achievable,
-                     "launch_ms": launch_ms, "timing": f"CUDA events around one {timing_mode} replay of "
-                                                       f"{args.steps} launches"},
-        "e2e": {"value": e2e_gf, "unit": "GF/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "steps": e2e_steps, "path": "txb_integrate_cells_host (pinned numpy in/out)"},
-        "gpu_launches": args.steps,
-        "clocks": sampler.summary(),
-    }
-    if world == 1 and not args.no_cpu:
-        r = cpu_reference(args.config, 3, target_s=args.cpu_seconds)
-        t = statistics.median(r["times"])
-        line["cpu_baseline"] = {"value": flops_cell * r["n"] / t / 1e9, "unit": "GF/s", "cores": r["cores"],
-                                "kind": r["kind"], "ms": t * 1e3,
-                                "sample": f"{r['n']} cells ({args.config}) x {len(r['times'])} passes, fork "
-                                          f"pool of {r['cores']} processes, median pass"}
-    if world == 1 and not args.no_variants:
-        variants = []
-        for v in VARIANTS:
-            vf, vb = config_model(v)
-            vw = rank_workload(v, 0, 1)
-            vs = max(4, -(-3 * L2_BYTES // (vb * vw["n"])) + 1)
-            steps = max(50, args.steps // 4) if vw["n"] <= (1 << 20) else 40
-            tot, _ = time_device(vw, steps, 5, min(vs, 64))  # sets x bytes > 3x L2
-            vl = tot / steps
-            variants.append({"config": v, "dtype": vw["dtype"], "cells": vw["n"],
-                             "gflops": vf * vw["n"] / (tot / steps * 1e-3) / 1e9,
-                             "gbs_launch": vb * vw["n"] / (vl * 1e-3) / 1e9,
-                             "frac": vb * vw["n"] / (vl * 1e-3) / 1e9 / peak, "launch_ms": vl,
-                             "bytes_per_cell": vb})
-            del vw
-            torch.cuda.empty_cache()
-        mesh_rows = []
-        for v in ("3d_varcoef_f64", "3d_varcoef_f32", "3d_elasticity_f64", "2d_varcoef_f64"):
-            vf, vb = config_model(v)
-            n = CONFIGS[v][3]
-            for given in (True, False):
-                ms, per_cell = time_mesh(v, max(50, args.steps // 4), 5, given_geometry=given)
-                mesh_rows.append({
-                    "config": ("mesh_given_geometry_" if given else "mesh_geometry_in_kernel_") + v,
-                    "path": "txb_integrate_mesh: gather" + ("" if given else " + float64 geometry") +
-                            " fused into the integration (replaces gather kernel + integrate_cells)",
-                    "cells": n, "launch_ms": ms, "gflops": vf * n / (ms * 1e-3) / 1e9,
-                    "gcells_per_s": n / (ms * 1e-3) / 1e9, "bytes_per_cell": per_cell,
-                    "gbs": per_cell * n / (ms * 1e-3) / 1e9, "frac": per_cell * n / (ms * 1e-3) / 1e9 / peak})
-            torch.cuda.empty_cache()
-        variants.extend(mesh_rows)
-        variants.extend(sweep_rows(peak))
-        variants.extend(api_rows())
-        variants.extend(jit_rows(peak, max(50, args.steps // 4)))
-        line["variants"] = variants
-    if strong is not None:
-        line["strong_scaling"] = strong
-    print(json.dumps(line), flush=True)
+        ent = json.loads(prof.read_text()).get("configs", {}).get(config)
+        if ent:
+            rd = ent["read_bytes_per_cell"] * n_cells
+            wr = ent["write_bytes_per_cell"] * n_cells
+            traffic = rd + wr
+            traffic_split = {"read": rd, "write": wr, "algorithmic": bytes_cell * n_cells,
+                             "ratio": (rd + wr) / (bytes_cell * n_cells), "source": ent.get("source")}
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic, "traffic_split": traffic_split,
+            "peak_source": peak_src, "bytes_per_cell": bytes_cell, "flops_per_cell_eq7": flops_cell,
+            "achievable_stream_gbs": achievable,
+            "frac_of_achievable": None if not achievable else achieved / achievable,
+            "launch_ms": launch_ms,
+            "timing": f"CUDA events on the launching stream around one {mode} replay of {steps} launches"}
 
 
 if __name__ == "__main__":

@@ -21,7 +21,8 @@ from .mesh import CellGeometry, FieldLayout, Mesh, compute_geometry, gather_coef
     generate_unit_simplex_mesh
 from .physics import CellAux, PhysicsForm, elasticity_form, poisson_form, poisson_varcoef_form
 
-__all__ = ["PHYSICS", "Workload", "refine_for", "make_workload"]
+__all__ = ["PHYSICS", "Workload", "refine_for", "make_workload", "kuhn_vertices", "kuhn_cells",
+           "uniform_slice"]
 
 # physics name -> (form factory, aux space)
 PHYSICS = {
@@ -37,6 +38,58 @@ def refine_for(dim: int, n_cells: int) -> int:
     while (2 * r * r if dim == 2 else 6 * r ** 3) < n_cells:
         r += 1
     return r
+
+
+def kuhn_vertices(dim: int, n: int) -> np.ndarray:
+    """Vertex coordinates of generate_unit_simplex_mesh(dim, n) (mesh.py), which
+    are cheap: (n+1)^dim rows against ~dim! n^dim cells."""
+    ticks = np.linspace(0.0, 1.0, n + 1)
+    m = n + 1
+    if dim == 2:
+        iy, ix = np.divmod(np.arange(m * m), m)
+        return np.column_stack([ticks[ix], ticks[iy]])
+    idx = np.arange(m ** 3)
+    return np.column_stack([ticks[idx % m], ticks[(idx // m) % m], ticks[idx // (m * m)]])
+
+
+def kuhn_cells(dim: int, n: int, lo: int, hi: int) -> np.ndarray:
+    """Rows [lo, hi) of generate_unit_simplex_mesh(dim, n).cells without
+    building the other rows: one rank's contiguous cell range (shard.cell_range)
+    of an N-GPU job costs O(hi - lo) host memory, not O(N x cells)."""
+    from .mesh import _CUBE_PERMS
+
+    m = n + 1
+    per = 2 if dim == 2 else 6
+    c = np.arange(lo, hi, dtype=np.int64)
+    sq, t = np.divmod(c, per)
+    if dim == 2:
+        sy, sx = np.divmod(sq, n)
+        v00 = sy * m + sx
+        v10, v01 = v00 + 1, v00 + m
+        v11 = v01 + 1
+        return np.ascontiguousarray(np.where((t == 0)[:, None], np.stack([v00, v10, v11], 1),
+                                             np.stack([v00, v11, v01], 1)))
+    corner = np.column_stack([sq // (n * n), (sq // n) % n, sq % n])
+    out = np.empty((hi - lo, 4), dtype=np.int64)
+    eye = np.eye(3, dtype=np.int64)
+    for k_t, (perm, parity) in enumerate(_CUBE_PERMS):
+        sel = t == k_t
+        cn = corner[sel]
+        p1 = cn + eye[perm[0]]
+        p2 = p1 + eye[perm[1]]
+        p3 = p2 + eye[perm[2]]
+        path = (cn, p1, p2, p3) if parity > 0 else (cn, p1, p3, p2)
+        for k, pt in enumerate(path):
+            out[sel, k] = (pt[:, 2] * m + pt[:, 1]) * m + pt[:, 0]
+    return out
+
+
+def uniform_slice(seed: int, lo: int, hi: int, low: float = 0.5, high: float = 1.5) -> np.ndarray:
+    """default_rng(seed).uniform(low, high, (N, 1))[lo:hi] without drawing the
+    first lo values: PCG64 jumps ahead lo outputs (one 64-bit draw per double)."""
+    bg = np.random.PCG64(seed)
+    bg.advance(lo)
+    return np.random.Generator(bg).uniform(low, high, (hi - lo, 1))
 
 
 @dataclass

@@ -36,6 +36,7 @@ sys.path.insert(0, str(REPO))
 
 L2_BYTES = 126 * 1024 * 1024
 FALLBACK_HBM_GBS = 6650.0
+METRIC = "element-integration GF/s (paper Eq.7 flops)"
 
 CONFIGS = {
     # name: (dim, physics, dtype, cells per GPU)

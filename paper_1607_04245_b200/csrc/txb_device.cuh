@@ -75,6 +75,40 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Cluster launch control (sm_100): a running CTA cancels a CTA of its own grid
+// that has not been launched yet and takes over its work -- hardware dynamic
+// scheduling with no global counter (nothing to reset, nothing shared between
+// launches, safe under CUDA-graph replay and concurrent streams).  The 16-byte
+// response lands in shared memory through the async proxy and completes a
+// transaction count of 16 bytes on `bar`.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void clc_try_cancel(void* resp16, uint64_t* bar) {
+  mbar_arrive_expect_tx(bar, 16);
+  asm volatile(
+      "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 [%0], [%1];" ::"r"(
+          smem_u32(resp16)),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+
+// The cancelled CTA's blockIdx.x, or -1 when no CTA was left to cancel (after
+// which no further request may be issued).
+__device__ __forceinline__ int64_t clc_cancelled_cta(const void* resp16) {
+  uint32_t ok, x;
+  asm volatile(
+      "{\n\t.reg .b128 r;\n\t.reg .pred p;\n\t"
+      "ld.shared.b128 r, [%2];\n\t"
+      "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p, r;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t"
+      "mov.u32 %1, 0;\n\t"
+      "@p clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 %1, r;\n\t}"
+      : "=r"(ok), "=r"(x)
+      : "r"(smem_u32(resp16))
+      : "memory");
+  return ok ? (int64_t)x : -1;
+}
+
 // L2 policy for streamed-once inputs: evict first, keep L2 for the outputs'
 // write-back and for the other CTAs' in-flight lines.
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {

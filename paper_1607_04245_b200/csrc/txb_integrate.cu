@@ -377,19 +377,9 @@ static int launch_t(bool zero_copy, const Config& c, const KernelInfo& k, const 
   a.n_bc = g.n_bc;
   a.stages = g.stages;
   a.warps = g.warps;
-  a.work = nullptr;
-  if (g.dynamic) {
-    unsigned long long* pool = work_pool_base();
-    if (!pool) return TXB_E_CUDA;
-    static std::atomic<uint64_t> seq{0};
-    a.work = pool + 2 * (seq.fetch_add(1) % WORK_POOL);
-    // deal ~TXB_STATIC_PCT % of the batches statically (whole rounds of the grid)
-    const int64_t n_batches = (n_cells + g.n_bc - 1) / g.n_bc;
-    const int pct = std::min(100, std::max(0, env_int("TXB_STATIC_PCT", 60)));
-    a.static_batches = n_batches * pct / 100 / g.grid * g.grid;
-  } else {
-    a.static_batches = 0;
-  }
+  a.dynamic = g.dynamic;
+  a.resident = g.resident;
+  a.static_batches = g.static_batches;
   // Bulk copies need 16-byte aligned, 16-byte sized slices for EVERY batch:
   // aligned base pointers and N_bc * (per-cell scalars) * sizeof(T) % 16 == 0
   // for each of the four arrays.  Otherwise every batch is read from global.

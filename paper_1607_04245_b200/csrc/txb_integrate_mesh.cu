@@ -38,7 +38,8 @@ struct MeshArgs {
   int warps;
   int bulk;
   int vec_coeffs;             // coeffs_global aligned to 2 scalars: paired loads for NCOMP 2 / 3
-  unsigned long long* work;
+  int dynamic;
+  int resident;
   int64_t static_batches;
   int prefetch;  // batches per CTA warmed into L2 before the programmatic-launch wait
   Tabulation<T> tab;
@@ -393,17 +394,9 @@ static int launch_mesh(const Config& c, const KernelInfo& k, const Geometry& g, 
                       sized16((int)sizeof(T)))) &&
            env_int("TXB_DISABLE_BULK", 0) == 0;
   a.vec_coeffs = ((uintptr_t)coeffs_global % (2 * sizeof(T))) == 0 && env_int("TXB_VEC_COEFFS", 1);
-  a.work = nullptr;
-  a.static_batches = 0;
-  if (g.dynamic) {
-    unsigned long long* pool = work_pool_base();
-    if (!pool) return TXB_E_CUDA;
-    static std::atomic<uint64_t> seq{0};
-    a.work = pool + 2 * (seq.fetch_add(1) % WORK_POOL);
-    const int64_t n_batches = (n_cells + g.n_bc - 1) / g.n_bc;
-    const int pct = std::min(100, std::max(0, env_int("TXB_STATIC_PCT", 60)));
-    a.static_batches = n_batches * pct / 100 / g.grid * g.grid;
-  }
+  a.dynamic = g.dynamic;
+  a.resident = g.resident;
+  a.static_batches = g.static_batches;
   a.prefetch = prefetch_batches(g);
   fill_tab(a.tab, c.n_q, c.dim + 1, c.dim, basis, basis_der, weights);
   void* params[] = {&a};

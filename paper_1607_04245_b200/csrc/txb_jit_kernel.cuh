@@ -342,9 +342,6 @@ __device__ __forceinline__ void integrate_body(const IntegrateArgs<real>& a, con
 }  // namespace jit
 }  // namespace txb
 
-// dynamic-scheduling counters of this module (zero at load, self-resetting)
-__device__ unsigned long long txb_jit_work_pool[4096][2];
-
 #ifndef TXB_JIT_MESH
 extern "C" __global__ void __launch_bounds__(txb::MAX_CTA_THREADS, 1)
 txb_jit_integrate(const __grid_constant__ txb::IntegrateArgs<real> a) {

@@ -18,10 +18,6 @@
 
 namespace txb {
 
-constexpr int WORK_POOL = 4096;  // per-launch dynamic-scheduling counters (device globals, zero at load)
-// one pool per translation unit (static): each kernel family draws its own slots
-static __device__ unsigned long long g_work_pool[WORK_POOL][2];
-
 // Byte layout of one ring stage: four 16-byte aligned regions holding the
 // batch's contiguous slices of inv_j, det_j, coeffs and aux.
 template <typename T, int D, int NCOMP, int AUX>
@@ -87,6 +83,11 @@ struct Geometry {
   int n_bl, n_cb, n_bc, n_t, threads, warps, stages, smem, grid;
   int64_t n_chunks, chunk_cells;
   bool dynamic;
+  // dynamic (cluster launch control): CTAs 0..resident-1 deal the first
+  // static_batches batches round-robin, CTA resident + j owns batch
+  // static_batches + j (txb_pipeline.cuh unit_batches)
+  int resident;
+  int64_t static_batches;
 };
 
 static int env_int(const char* name, int dflt) {
@@ -223,6 +224,25 @@ static DeviceProps device_props(int dev) {
   return cache[dev];
 }
 
+// The kernel's dynamic shared-memory limit is raised ONCE per (function,
+// device) to the device's opt-in maximum and never lowered, so launches of
+// the same kernel with different stage sizes from concurrent threads cannot
+// race on the attribute (each launch passes its own size).
+static bool allow_max_smem(void* fn, int dev, int smem_cap) {
+  static std::mutex mu;
+  static std::map<std::pair<void*, int>, bool> done;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair(fn, dev);
+  if (done.count(key)) return true;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap);
+  if (e != cudaSuccess) {
+    cuda_fail(e, "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
+    return false;
+  }
+  done[key] = true;
+  return true;
+}
+
 static int compute_geometry(const Config& c, const KernelInfo& k, int64_t n_cells, int n_bl, int n_cb,
                             bool query_device, Geometry& g) {
   default_decomposition(c, k.family, n_cells, n_bl, n_cb);
@@ -263,14 +283,14 @@ static int compute_geometry(const Config& c, const KernelInfo& k, int64_t n_cell
   // ramp (measured, profiles/r1_sweep.md).  TXB_STAGES forces a depth.
   const int forced = env_int("TXB_STAGES", 0);
   const int64_t inflight_target = (int64_t)env_int("TXB_INFLIGHT_KB", tuned_inflight_kb(c, k.family, n_cells)) * 1024;
+  if (query_device && !allow_max_smem(k.fn, dev, smem_cap)) return TXB_E_CUDA;
   auto occupancy = [&](int smem) {
     int occ = 1;
     if (query_device) {
-      static std::mutex mu;
-      std::lock_guard<std::mutex> lk(mu);
-      cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.fn, g.threads, smem) != cudaSuccess || occ < 1)
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.fn, g.threads, smem) != cudaSuccess || occ < 1) {
+        cudaGetLastError();
         occ = 1;
+      }
     } else {
       occ = std::max(1, std::min(2048 / g.threads, smem_cap / std::max(smem, 1)));
     }
@@ -324,11 +344,6 @@ static int compute_geometry(const Config& c, const KernelInfo& k, int64_t n_cell
   }
   g.stages = best_s;
   g.smem = fixed + best_s * stage;
-  if (query_device) {
-    static std::mutex mu2;
-    std::lock_guard<std::mutex> lk(mu2);
-    cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem);
-  }
   const int64_t resident = (int64_t)occ * sms;
   if (n_cb > 0) {
     // paper mode: chunks of N_cb batches, round-robin over the CTAs
@@ -342,37 +357,33 @@ static int compute_geometry(const Config& c, const KernelInfo& k, int64_t n_cell
   }
   g.n_chunks = (n_cells + g.chunk_cells - 1) / g.chunk_cells;
   g.grid = (int)std::max<int64_t>(1, std::min<int64_t>(g.n_chunks, resident));
-  // Default: dynamic batch scheduling (a per-launch atomic counter) so CTAs on
-  // SMs that get more bandwidth take more batches and all finish together.
-  // An explicit n_cb keeps the paper's static chunk order.
-  // Only worth it when a batch is long enough to hide the counter's atomic
-  // latency (>= 10 KB per stage; measured, profiles/r1_sweep.md).
+  // Default: dynamic batch scheduling so CTAs on SMs that get more bandwidth
+  // take more batches and all finish together.  An explicit n_cb keeps the
+  // paper's static chunk order.  Only worth it when a batch is long enough to
+  // hide the scheduling request's latency (>= 10 KB per stage; measured with
+  // an atomic counter in round 1, profiles/r1_sweep.md).
   const int dyn_env = env_int("TXB_DYNAMIC", -1);
   g.dynamic = n_cb <= 0 && (dyn_env < 0 ? stage >= 10 * 1024 : dyn_env != 0);
+  g.resident = 0;
+  g.static_batches = 0;
   if (g.dynamic) {
+    // One CTA per scheduling unit; the resident CTAs cancel the grid's
+    // not-yet-launched CTAs and run their units (cluster launch control), so
+    // the grid stays persistent in effect.  ~TXB_STATIC_PCT % of the batches
+    // (whole rounds of the resident grid) are dealt round-robin first.
     const int64_t n_batches = (n_cells + g.n_bc - 1) / g.n_bc;
-    g.grid = (int)std::max<int64_t>(1, std::min<int64_t>(n_batches, resident));
+    const int64_t r = std::max<int64_t>(1, std::min<int64_t>(n_batches, resident));
+    const int pct = std::min(100, std::max(0, env_int("TXB_STATIC_PCT", 60)));
+    g.static_batches = n_batches * pct / 100 / r * r;
+    g.resident = g.static_batches > 0 ? (int)r : 0;
+    const int64_t units = g.resident + (n_batches - g.static_batches);
+    if (units > 0x7fffffff) {
+      set_error("%lld batches exceed the grid limit", (long long)n_batches);
+      return TXB_E_CONFIG;
+    }
+    g.grid = (int)std::max<int64_t>(1, units);
   }
   return TXB_OK;
-}
-
-// Device address of the dynamic-scheduling counter pool on the current device.
-static unsigned long long* work_pool_base() {
-  static std::mutex mu;
-  static std::vector<unsigned long long*> cache;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-  std::lock_guard<std::mutex> lk(mu);
-  if ((int)cache.size() <= dev) cache.resize(dev + 1, nullptr);
-  if (!cache[dev]) {
-    void* p = nullptr;
-    if (cudaGetSymbolAddress(&p, g_work_pool) != cudaSuccess) {
-      cuda_fail(cudaGetLastError(), "cudaGetSymbolAddress(g_work_pool)");
-      return nullptr;
-    }
-    cache[dev] = (unsigned long long*)p;
-  }
-  return cache[dev];
 }
 
 // Debug timeline (txb_debug_trace): consecutive launches on this thread take

@@ -45,8 +45,9 @@ struct IntegrateArgs {
   int stages;  // ring depth
   int warps;   // consumer warps
   int bulk;    // 1: full batches arrive by bulk copy; 0: every batch read from global
-  unsigned long long* work;  // dynamic mode: {next batch, CTAs done}, self-resetting; NULL = static chunks
-  int64_t static_batches;    // dynamic mode: batches dealt round-robin before the counter takes over
+  int dynamic;               // 1: cluster-launch-control scheduling (units below); 0: static chunks
+  int resident;              // dynamic: CTAs 0..resident-1 own the round-robin share of the first
+  int64_t static_batches;    //   static_batches batches; CTA resident + j owns batch static_batches + j
   int prefetch;              // batches per CTA warmed into L2 before the programmatic-launch wait
   unsigned long long* trace; // debug (txb_debug_trace): 4 %globaltimer stamps per CTA, NULL = off
   Tabulation<T> tab;
@@ -113,10 +114,11 @@ __device__ __forceinline__ void load_row(const T* __restrict__ p, T (&r)[N]) {
 // ---------------------------------------------------------------------------
 // The batch pipeline shared by every streaming kernel of the library.
 //
-// Args provides: n_cells, n_chunks, chunk_cells, n_bc, stages, warps, work,
-// static_batches.  One producer lane (warp `warps`, lane 0) walks the batch
-// sequence -- static contiguous chunks, or round-robin + a per-launch atomic
-// counter for the tail (`work` != NULL) -- and for each batch calls
+// Args provides: n_cells, n_chunks, chunk_cells, n_bc, stages, warps,
+// dynamic, resident, static_batches.  One producer lane (warp `warps`, lane 0)
+// walks the batch sequence -- static contiguous chunks, or (dynamic) its own
+// scheduling unit and then the units of the CTAs it cancels through cluster
+// launch control -- and for each batch calls
 //     issue(stage_ptr, c0, ncell, full_bar)  -> true if it posted expect_tx and
 //                                              bulk copies, false if the batch
 //                                              must be read from global memory
@@ -129,30 +131,33 @@ struct PipelineSmem {
   uint64_t* full;
   uint64_t* empty;
   int64_t* info_c0;
+  uint64_t* clc_bar;        // cluster-launch-control response barrier
+  unsigned char* clc_resp;  // 16-byte response (16-byte aligned)
   int* info_n;
-  int* warps_done;
 };
 
-// mbarriers + stage info + done counter, carved after `base`
+// mbarriers + stage info + the launch-control response, carved after `base`
+// (16-byte aligned)
 __device__ __forceinline__ PipelineSmem carve_pipeline(unsigned char* base) {
   PipelineSmem p;
   p.full = reinterpret_cast<uint64_t*>(base);
   p.empty = p.full + MAX_STAGES;
   p.info_c0 = reinterpret_cast<int64_t*>(p.empty + MAX_STAGES);
-  p.info_n = reinterpret_cast<int*>(p.info_c0 + MAX_STAGES);
-  p.warps_done = p.info_n + MAX_STAGES;
+  p.clc_bar = reinterpret_cast<uint64_t*>(p.info_c0 + MAX_STAGES);
+  p.clc_resp = reinterpret_cast<unsigned char*>(p.clc_bar + 2);
+  p.info_n = reinterpret_cast<int*>(p.clc_resp + 16);
   return p;
 }
-constexpr int PIPELINE_SMEM_BYTES = 8 * (3 * MAX_STAGES) + 4 * MAX_STAGES + 16;
+constexpr int PIPELINE_SMEM_BYTES = 8 * (3 * MAX_STAGES) + 16 + 16 + 4 * MAX_STAGES;
 
 template <class Args>
 __device__ __forceinline__ void pipeline_init(const Args& a, const PipelineSmem& p) {
   if (threadIdx.x == 0) {
-    *p.warps_done = 0;
     for (int s = 0; s < a.stages; ++s) {
       mbar_init(&p.full[s], 1);
       mbar_init(&p.empty[s], a.warps * EMPTY_ARRIVALS_PER_WARP);
     }
+    mbar_init(p.clc_bar, 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -160,15 +165,34 @@ __device__ __forceinline__ void pipeline_init(const Args& a, const PipelineSmem&
 
 // First cells of this CTA's first `count` batches (for L2 prefetch before the
 // programmatic-launch wait): calls f(c0, ncell) for each.
+// Dynamic mode, the batches of scheduling unit u (a CTA index of the grid):
+// u < resident: batches u, u + resident, ... below static_batches (dealt
+// round-robin, so the whole grid sweeps the arrays together); u >= resident:
+// the single batch static_batches + (u - resident).  f(c0, ncell) per batch
+// until f returns false.
+template <class Args, class F>
+__device__ __forceinline__ void unit_batches(const Args& a, int64_t u, F f) {
+  const int nbc = a.n_bc;
+  if (u < a.resident) {
+    for (int64_t b = u; b < a.static_batches; b += a.resident) {
+      const int64_t c0 = b * nbc;
+      if (!f(c0, (int)min((int64_t)nbc, a.n_cells - c0))) return;
+    }
+  } else {
+    const int64_t c0 = (a.static_batches + (u - a.resident)) * nbc;
+    if (c0 < a.n_cells) f(c0, (int)min((int64_t)nbc, a.n_cells - c0));
+  }
+}
+
 template <class Args, class F>
 __device__ __forceinline__ void pipeline_first_batches(const Args& a, int count, F f) {
-  const int nbc = a.n_bc;
-  if (a.work) {
-    for (int64_t b = blockIdx.x; count > 0 && b < a.static_batches; b += gridDim.x, --count) {
-      const int64_t c0 = b * nbc;
-      f(c0, (int)min((int64_t)nbc, a.n_cells - c0));
-    }
+  if (a.dynamic) {
+    unit_batches(a, blockIdx.x, [&](int64_t c0, int ncell) {
+      f(c0, ncell);
+      return --count > 0;
+    });
   } else if ((int64_t)blockIdx.x < a.n_chunks) {
+    const int nbc = a.n_bc;
     const int64_t lo = (int64_t)blockIdx.x * a.chunk_cells;
     const int64_t hi = min(a.n_cells, lo + a.chunk_cells);
     for (int64_t c0 = lo; count > 0 && c0 < hi; c0 += nbc, --count) f(c0, (int)min((int64_t)nbc, hi - c0));
@@ -217,22 +241,27 @@ __device__ __forceinline__ void pipeline_produce(const Args& a, const PipelineSm
       phase ^= 1;
     }
   };
-  if (a.work) {
-    // dynamic: the first a.static_batches batches are dealt round-robin,
-    // the rest are grabbed from a per-launch counter so CTAs on SMs that
-    // get more bandwidth take more of the tail.  The next grab is issued
-    // before the current batch is published, hiding the atomic's latency.
-    const int64_t n_batches = (a.n_cells + nbc - 1) / nbc;
-    for (int64_t b = blockIdx.x; b < a.static_batches; b += gridDim.x) {
-      const int64_t c0 = b * nbc;
-      publish(c0, (int)min((int64_t)nbc, a.n_cells - c0));
-    }
-    int64_t next = a.static_batches + (int64_t)atomicAdd(a.work, 1ull);
-    while (next < n_batches) {
-      const int64_t b = next;
-      next = a.static_batches + (int64_t)atomicAdd(a.work, 1ull);
-      const int64_t c0 = b * nbc;
-      publish(c0, (int)min((int64_t)nbc, a.n_cells - c0));
+  if (a.dynamic) {
+    // Cluster launch control: run this CTA's own unit, then keep cancelling
+    // CTAs of the grid that have not launched yet and run their units, until
+    // none is left.  One request is always in flight ahead of the unit being
+    // published, hiding its latency; none is issued after a failed one.
+    clc_try_cancel(p.clc_resp, p.clc_bar);
+    uint32_t clc_phase = 0;
+    unit_batches(a, blockIdx.x, [&](int64_t c0, int ncell) {
+      publish(c0, ncell);
+      return true;
+    });
+    for (;;) {
+      mbar_wait(p.clc_bar, clc_phase);
+      clc_phase ^= 1;
+      const int64_t u = clc_cancelled_cta(p.clc_resp);
+      if (u < 0) break;
+      clc_try_cancel(p.clc_resp, p.clc_bar);
+      unit_batches(a, u, [&](int64_t c0, int ncell) {
+        publish(c0, ncell);
+        return true;
+      });
     }
   } else {
     // static: contiguous chunks, round-robin over the CTAs
@@ -271,17 +300,7 @@ __device__ __forceinline__ void pipeline_consume(const Args& a, const PipelineSm
       phase ^= 1;
     }
   }
-  // dynamic mode: the last CTA out resets the per-launch counters for the
-  // next launch that draws this slot (stream order / PDL wait make it visible)
-  if (a.work && lane == 0) {
-    if (atomicAdd(p.warps_done, 1) == a.warps - 1) {
-      __threadfence();
-      if (atomicAdd(a.work + 1, 1ull) == (unsigned long long)gridDim.x - 1) {
-        atomicExch(a.work, 0ull);
-        atomicExch(a.work + 1, 0ull);
-      }
-    }
-  }
+  (void)lane;
 }
 
 }  // namespace txb

@@ -245,6 +245,13 @@ def integrate_transposed(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule:
         elem = integrate_cells(
             tab, rule, CellGeometry(_dev(cell_geom.inv_jacobians, torch, dt), _dev(cell_geom.determinants, torch, dt)),
             blocks, aux_dev, form, dtype=dt, n_bl=n_bl, n_cb=n_cb)
+    if geom.n_r and dt == np.float32:
+        # executor.py:258-264: the remainder cells (n mod N_chunk) are integrated
+        # in float64 and cast -- here by the float64 kernels (bit-identical to
+        # integrate_reference), so the f32 residual equals the reference's bits
+        span = geom.n_chunks * geom.n_chunk
+        elem[span:] = _remainder_f64(mesh, layout, tab, rule, form, kernel, glob, aux, cell_geom, cells_dev,
+                                     verts_dev, span, n_bl).to(elem.dtype)
     residual = scatter_add_element_vectors(mesh, layout, elem, incidence=_incidence_for(mesh, cells_dev))
 
     trace = ExecutionTrace.uniform(geom, dt.itemsize, model_batch_counters(geom, form, dt.itemsize, aux),
@@ -259,6 +266,48 @@ def integrate_transposed(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule:
 _FUSABLE: dict = {}
 
 
+def _remainder_f64(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: QuadratureRule, form: PhysicsForm,
+                   kernel, glob, aux: Optional[CellAux], cell_geom: Optional[CellGeometry], cells_dev, verts_dev,
+                   span: int, n_bl: int):
+    """Element vectors of cells [span, n) in float64 (a CUDA tensor): the
+    reference's remainder path (integrate_reference on float64 geometry,
+    coefficients and aux, executor.py:258-264) on the float64 kernels."""
+    torch = _torch()
+    f64 = np.dtype(np.float64)
+    n = mesh.n_cells
+    sub = Mesh(mesh.dim, mesh.vertices, mesh.cells[span:])
+    cells = cells_dev[span:]
+    g64 = _dev(glob, torch, f64)
+    a64 = None if aux is None else CellAux(aux.space, _dev(aux.values[span:n], torch, f64))
+    cg = None
+    if cell_geom is not None:
+        cg = CellGeometry(_dev(cell_geom.inv_jacobians[span:n], torch, f64),
+                          _dev(cell_geom.determinants[span:n], torch, f64))
+    k64 = _resolve_backend(None, form, rule.n_q, aux, 8)
+    if _mesh_fusable(tab, rule) and not isinstance(k64, _backend.JitKernel):
+        return integrate_mesh(sub, layout, tab, rule, form, g64, a64, dtype=f64, cell_geom=cg, cells=cells,
+                              vertices=verts_dev, n_bl=n_bl)
+    if isinstance(k64, _backend.JitKernel) and cg is None and os.environ.get("TXB_JIT_MESH", "1") != "0":
+        return _jit_mesh(k64, sub, tab, rule, form, g64, a64, f64, cells, verts_dev, n_bl)
+    if cg is None:
+        cg = compute_geometry(sub, cells=cells, vertices=verts_dev, device_out=True)
+    blocks = gather_coefficients(sub, layout, g64, cells=cells)
+    return integrate_cells(tab, rule, CellGeometry(_dev(cg.inv_jacobians, torch, f64), _dev(cg.determinants, torch, f64)),
+                           blocks, a64, form, dtype=f64, n_bl=n_bl)
+
+
+def _check_aux_shape(aux, n_cells: int, n_b: int, form: PhysicsForm):
+    """The full shape of a CellAux's values: (n, n_aux) for p0, (n, n_b, n_aux)
+    for p1 -- the reference's memoryviews reject anything else
+    (_kernels_cy.pyx:37-49); the fused kernels would read out of bounds."""
+    if aux is None:
+        return
+    want = (n_cells, form.n_aux) if aux.space == "p0" else (n_cells, n_b, form.n_aux)
+    got = tuple(int(x) for x in aux.values.shape)
+    if got != want:
+        raise ShapeError(f"{aux.space} auxiliary values have shape {got}, expected {want}")
+
+
 def _jit_mesh(kernel, mesh: Mesh, tab: Tabulation, rule: QuadratureRule, form: PhysicsForm, glob_dev, aux_dev, dt,
               cells_dev, verts_dev, n_bl: int):
     """Element vectors of a run-time compiled form straight from the mesh
@@ -271,6 +320,7 @@ def _jit_mesh(kernel, mesh: Mesh, tab: Tabulation, rule: QuadratureRule, form: P
 
     torch = _torch()
     n = mesh.n_cells
+    _check_aux_shape(aux_dev, n, tab.n_b, form)
     if int(glob_dev.numel()) != mesh.n_vertices * form.n_comp:
         raise ShapeError(f"global vector has {glob_dev.numel()} entries, expected {mesh.n_vertices * form.n_comp}")
     res = torch.empty((n, tab.n_b, form.n_comp), dtype=glob_dev.dtype, device="cuda")
@@ -333,6 +383,7 @@ def integrate_mesh(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: Quadr
         raise ValueError(f"the fused mesh kernel covers the shipped forms; form {form.name!r} runs through "
                          "integrate_transposed (geometry -> gather -> run-time compiled integration)")
     n = mesh.n_cells
+    _check_aux_shape(aux, n, tab.n_b, form)
     C = cells if cells is not None else torch.from_numpy(np.ascontiguousarray(mesh.cells, dtype=np.int64)).cuda()
     X = vertices if vertices is not None else \
         torch.from_numpy(np.ascontiguousarray(mesh.vertices, dtype=np.float64)).cuda()

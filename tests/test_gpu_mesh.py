@@ -276,7 +276,9 @@ def test_random_mesh_residual_bitwise(dim, refine, form_i, dtype, given_geom, tw
                                       shared_mem_limit=None, cell_geom=cg)
     fc = {"poisson": 0, "poisson_varcoef": 1, "elasticity": 2}[form.name]
     am = {None: 0, "p0": 1, "p1": 2}[aux_space]
-    elem = oracle.integrate(fc, am, tab.basis, tab.basis_der, rule.weights, inv, det,
-                            oracle.gather(mesh.cells, glob, form.n_comp), None if aux is None else aux.values, npdt)
+    g = txb.derive_execution_geometry(dim, tab.n_b, form.n_comp, rule.n_q, 8, 2, mesh.n_cells)
+    elem = oracle.integrate_with_remainder(fc, am, tab.basis, tab.basis_der, rule.weights, inv, det,
+                                           oracle.gather(mesh.cells, glob, form.n_comp),
+                                           None if aux is None else aux.values, npdt, g.n_chunks * g.n_chunk)
     want = oracle.scatter_add(mesh.cells, elem, mesh.n_vertices)
     assert bitwise_equal(res, want)

@@ -284,6 +284,13 @@ def test_integrate_transposed_user_forms_mesh_fused(name, dim, dtype):
                                       tab.basis_der, rule.weights, inv, det,
                                       oracle.gather(mesh.cells, glob, s["n_comp"]),
                                       None if aux is None else aux.values, npdt)
+        g = txb.derive_execution_geometry(dim, tab.n_b, s["n_comp"], rule.n_q, 8, 2, mesh.n_cells)
+        sp = g.n_chunks * g.n_chunk
+        if sp < mesh.n_cells and npdt == np.float32:  # remainder: float64 then cast (executor.py:258-264)
+            elem[sp:] = oracle.integrate_forms(s["f1_many"], s["f0_many"], s["uses_grad_a"], s["aux"], tab.basis,
+                                               tab.basis_der, rule.weights, inv[sp:], det[sp:],
+                                               oracle.gather(mesh.cells[sp:], glob, s["n_comp"]),
+                                               None if aux is None else aux.values[sp:], np.float64).astype(npdt)
         want = oracle.scatter_add(mesh.cells, elem, mesh.n_vertices)
         assert bitwise_equal(res, want), (rule.n_q, dtype)
         res2, _ = txb.integrate_transposed(mesh, layout, tab, rule, f, glob, aux, n_bl=8, n_cb=2, dtype=dtype,

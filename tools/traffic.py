@@ -14,7 +14,7 @@ separately:
           nothing; a sweep-only range is measured as the baseline).
 
 Usage (on the GPU box; both runs execute the same script):
-  ncu --replay-mode range --profile-from-start off --metrics M --csv \
+  ncu --replay-mode range --metrics M --csv \
       --log-file gpurun_out/TAG_traffic_range.csv  python tools/traffic.py run
   ncu --profile-from-start off --cache-control all --clock-control none \
       -k regex:integrate --metrics M --csv \

@@ -10,6 +10,14 @@ never runs this: it only reads the committed outputs
   tests/golden/user_cases.npz    user physics forms (f0, several aux fields,
                                  grad a; oracle/user_forms.py) through the
                                  reference's python lane, f64 and f32
+  tests/golden/residual_cases.npz  mesh-level residuals of the reference's own
+                                 txfem.integrate_transposed (executor.py:161-267):
+                                 f32 / f64, remainder cells n_r > 0 (float64
+                                 + cast in the reference), every shipped form,
+                                 midpoint and two-point rules, perturbed
+                                 meshes with shuffled numbering
+  tests/golden/residual_hashes.json  sha256 of larger integrate_transposed
+                                 residuals (84k-cell 3D meshes)
 
 Every output here comes from the reference itself:
   * ``ref_f64``  txfem.reference.integrate_reference (reference.py:40-112)
@@ -26,7 +34,7 @@ Input conventions follow the reference tests and CLI:
   * random near-identity Jacobians J = I + 0.2 U(-1,1)
     (tests/test_executor.py:273-280).
 
-Usage:  python tests/golden/make_golden.py [user]   (user: only user_cases.npz)
+Usage:  python tests/golden/make_golden.py [user|residual]   (only user_cases.npz / the residual goldens)
 """
 
 from __future__ import annotations
@@ -288,12 +296,94 @@ def user_cases():
     return arrays
 
 
+RESIDUAL_FORMS = ["poisson", "varcoef_p0", "varcoef_p1", "elasticity"]
+
+
+def residual_problem(dim, refine, physics, seed):
+    """A perturbed Kuhn mesh with a shuffled vertex numbering and cell order,
+    N(0,1) global coefficients, the form's aux (reference conventions)."""
+    rng = np.random.default_rng(seed)
+    base = txfem.generate_unit_simplex_mesh(dim, refine)
+    perm = rng.permutation(base.n_vertices)
+    verts = base.vertices[np.argsort(perm)] + (0.15 / refine) * rng.uniform(-1, 1, base.vertices.shape)
+    cells = perm[base.cells][rng.permutation(base.n_cells)]
+    mesh = Mesh(dim=dim, vertices=np.ascontiguousarray(verts), cells=np.ascontiguousarray(cells))
+    factory, aux_space = FORMS[physics]
+    form = factory(dim)
+    layout = txfem.FieldLayout(n_comp=form.n_comp)
+    glob = rng.standard_normal(layout.global_size(mesh))
+    aux = None
+    if aux_space == "p0":
+        aux = CellAux("p0", rng.uniform(0.5, 1.5, (mesh.n_cells, 1)))
+    elif aux_space == "p1":
+        aux = CellAux("p1", rng.uniform(0.5, 1.5, (mesh.n_vertices, 1))[mesh.cells])
+    return mesh, form, layout, glob, aux
+
+
+def residual_cases():
+    """integrate_transposed of the reference (default lane: compiled) with
+    n_bl / n_cb chosen so n mod N_chunk > 0."""
+    arrays, index = {}, []
+    for dim, refine in ((2, 9), (3, 4)):
+        for physics in RESIDUAL_FORMS:
+            for n_q in (1, 2):
+                seed = 100 * dim + 10 * RESIDUAL_FORMS.index(physics) + n_q
+                mesh, form, layout, glob, aux = residual_problem(dim, refine, physics, seed)
+                rule = txfem.quadrature_rule(dim, 1) if n_q == 1 else txfem.two_point_rule(dim)
+                tab = txfem.tabulate(dim, rule)
+                n_bl, n_cb = 5, 3
+                g = txfem.derive_execution_geometry(dim, tab.n_b, form.n_comp, rule.n_q, n_bl, n_cb, mesh.n_cells)
+                assert g.n_r > 0 and g.n_chunks > 0
+                name = f"{dim}d_{physics}_q{n_q}"
+                for dt in ("f64", "f32"):
+                    res, trace = txfem.integrate_transposed(mesh, layout, tab, rule, form, glob, aux, n_bl=n_bl,
+                                                            n_cb=n_cb, dtype=dt, shared_mem_limit=None)
+                    assert trace.remainder_cells == g.n_r
+                    arrays[f"{name}/res_{dt}"] = res
+                arrays[f"{name}/vertices"] = mesh.vertices
+                arrays[f"{name}/cells"] = mesh.cells
+                arrays[f"{name}/glob"] = glob
+                if aux is not None:
+                    arrays[f"{name}/aux"] = aux.values
+                meta = dict(dim=dim, physics=physics, n_q=n_q, n_bl=n_bl, n_cb=n_cb, n_r=g.n_r,
+                            span=g.n_chunks * g.n_chunk, aux=None if aux is None else aux.space)
+                arrays[f"{name}/meta"] = np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8)
+                index.append(name)
+    arrays["index"] = np.frombuffer(json.dumps(index).encode(), dtype=np.uint8)
+    return arrays
+
+
+def residual_hashes():
+    """Larger residuals by hash: 3D refine 24 (82,944 cells), seeded as
+    residual_problem, midpoint rule, n_bl = 32 / n_cb = 7 (n_r > 0)."""
+    out = {}
+    for physics in ("varcoef_p0", "elasticity"):
+        mesh, form, layout, glob, aux = residual_problem(3, 24, physics, 7)
+        rule = txfem.quadrature_rule(3, 1)
+        tab = txfem.tabulate(3, rule)
+        g = txfem.derive_execution_geometry(3, tab.n_b, form.n_comp, 1, 32, 7, mesh.n_cells)
+        ent = {"n_cells": mesh.n_cells, "n_r": g.n_r, "inputs": sha(np.concatenate(
+            [mesh.vertices.ravel(), mesh.cells.ravel().astype(np.float64), glob]
+            + ([aux.values.ravel()] if aux is not None else [])))}
+        for dt in ("f64", "f32"):
+            res, _ = txfem.integrate_transposed(mesh, layout, tab, rule, form, glob, aux, n_bl=32, n_cb=7,
+                                                dtype=dt, shared_mem_limit=None)
+            ent[dt] = sha(res)
+        out[f"3d_{physics}_refine24"] = ent
+    return out
+
+
 def _tables(rule, dim):
     tab = txfem.tabulate(dim, rule)
     return tab.basis, tab.basis_der, rule.weights
 
 
 def main():
+    if sys.argv[1:] == ["residual"]:
+        np.savez_compressed(OUT / "residual_cases.npz", **residual_cases())
+        (OUT / "residual_hashes.json").write_text(json.dumps(residual_hashes(), indent=1) + "\n")
+        print("wrote", OUT / "residual_cases.npz", OUT / "residual_hashes.json")
+        return
     if sys.argv[1:] == ["user"]:
         np.savez_compressed(OUT / "user_cases.npz", **user_cases())
         print("wrote", OUT / "user_cases.npz")
@@ -302,7 +392,9 @@ def main():
     arrays = small_cases()
     np.savez_compressed(OUT / "small_cases.npz", **arrays)
     (OUT / "big_hashes.json").write_text(json.dumps(big_hashes(), indent=1) + "\n")
-    print("wrote", OUT / "small_cases.npz", OUT / "big_hashes.json")
+    np.savez_compressed(OUT / "residual_cases.npz", **residual_cases())
+    (OUT / "residual_hashes.json").write_text(json.dumps(residual_hashes(), indent=1) + "\n")
+    print("wrote", OUT / "small_cases.npz", OUT / "big_hashes.json", OUT / "residual_cases.npz")
 
 
 if __name__ == "__main__":

@@ -42,21 +42,23 @@ TO_NS = {"nsecond": 1.0, "ns": 1.0, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "
 
 
 def run(configs):
-    import ctypes
-
     import numpy as np
     import torch
 
     import bench
-    from paper_1607_04245_b200 import _lib, backend
+    from paper_1607_04245_b200 import backend
 
     torch.cuda.set_device(0)
-    L = _lib.lib()
     sweep = torch.ones(SWEEP_BYTES, dtype=torch.uint8, device="cuda")
-    s = torch.cuda.current_stream()
 
-    def flush():  # read-only sweep: evicts (writes back) every dirty L2 line, writes nothing itself
-        _lib.check(L.txb_stream_probe(sweep.data_ptr(), SWEEP_BYTES, None, 0, ctypes.c_void_p(s.cuda_stream)))
+    words = sweep.view(torch.int64)
+    acc = torch.zeros((), dtype=torch.int64, device="cuda")
+
+    def flush():
+        # read sweep with DEFAULT-policy loads (a torch reduction): it evicts --
+        # writes back -- every dirty L2 line; evict-first (.cs) loads would only
+        # recycle their own lines and leave the launch's outputs dirty in L2
+        torch.sum(words, out=acc)
 
     for name in configs:
         wl = bench.rank_workload(name, 0, 1)

@@ -54,6 +54,12 @@ def active_backend() -> str:
     return "cuda"
 
 
+def compiled_available() -> bool:
+    """The reference's question (backend.py:30-31): is ITS compiled CPU lane
+    here?  Never -- this framework's lane is "cuda" (cuda_available())."""
+    return False
+
+
 class JitKernel:
     """A run-time compiled integration kernel (process-lifetime handle)."""
 

@@ -72,16 +72,21 @@ put_kernel(int64_t n_send, int n_comp, int rank, const int64_t* __restrict__ sen
                                      (int64_t)(epoch & 1) * slot_bytes[p]);
       slot[send_dst[i] * n_comp + c] = elem[send_rows[i] * n_comp + c];  // P2P store into the owner's window
     }
+  } else if (threadIdx.x == 0) {
+    atomicExch(&mine->put_failed[epoch & 1], 1u);  // this CTA skipped its stores
   }
-  __threadfence_system();  // this CTA's stores before its completion count
+  __threadfence_system();  // this CTA's stores (or failure mark) before its completion count
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned int* ctr = &mine->counters[epoch & 1];
     if (atomicAdd(ctr, 1u) == gridDim.x - 1) {
       __threadfence_system();
       atomicExch(ctr, 0u);  // reused at epoch + 2 (stream order)
-      for (int i = 0; i < n_out_peers; ++i)
-        store_release_sys(&header(windows[out_peers[i]])->flags[rank], epoch);
+      // a failed put still publishes the epoch (the receivers must not wait
+      // out their own timeout), but poisoned: they report error 3 instead of
+      // assembling rows that never arrived
+      const unsigned long long flag = atomicExch(&mine->put_failed[epoch & 1], 0u) ? (epoch | POISON) : epoch;
+      for (int i = 0; i < n_out_peers; ++i) store_release_sys(&header(windows[out_peers[i]])->flags[rank], flag);
     }
   }
 }
@@ -95,42 +100,56 @@ assemble_kernel(int64_t n_owned, const int64_t* __restrict__ offsets, const int3
   WindowHeader* mine = header(windows[rank]);
   const T* recv = reinterpret_cast<const T*>(static_cast<const unsigned char*>(windows[rank]) + HEADER_BYTES +
                                              (int64_t)(epoch & 1) * my_slot_bytes);
+  __shared__ int bad;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < n_in_peers; ++i)
-      if (!wait_at_least(&mine->flags[in_peers[i]], epoch, timeout_ns)) {
-        atomicCAS(&mine->error, 0, 2);
+    bad = 0;
+    for (int i = 0; i < n_in_peers; ++i) {
+      const unsigned long long f = wait_flag(&mine->flags[in_peers[i]], epoch, timeout_ns);
+      if (f == 0 || (f & POISON)) {  // timed out, or the sender's put failed
+        atomicCAS(&mine->error, 0, f == 0 ? 2 : 3);
+        bad = 1;
         break;
       }
+    }
   }
   __syncthreads();
-  constexpr int U = 8;
-  const int64_t n = n_owned * NC;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < n; o += stride) {
-    const int64_t v = NC == 1 ? o : o / NC;
-    const int k = NC == 1 ? 0 : (int)(o - v * NC);
-    int64_t e = offsets[v];
-    const int64_t end = offsets[v + 1];
-    T sum = T(0);  // +0, then every row in (rank, cell) order: np.add.at's chain
-    for (; e < end; e += U) {
-      int32_t idx[U];
+  if (bad) {
+    // never a silently wrong residual: the owned entries become NaN, the error
+    // stays in the window (PeerHalo.check), and the epoch is NOT acked, so the
+    // senders fail too instead of overwriting the slot
+    const int64_t n = n_owned * NC;
+    for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x)
+      out[o] = T(__longlong_as_double(0x7ff8000000000000ll));
+  } else {
+    constexpr int U = 8;
+    const int64_t n = n_owned * NC;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < n; o += stride) {
+      const int64_t v = NC == 1 ? o : o / NC;
+      const int k = NC == 1 ? 0 : (int)(o - v * NC);
+      int64_t e = offsets[v];
+      const int64_t end = offsets[v + 1];
+      T sum = T(0);  // +0, then every row in (rank, cell) order: np.add.at's chain
+      for (; e < end; e += U) {
+        int32_t idx[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) idx[u] = e + u < end ? __ldg(incidence + e + u) : -1;
-      T val[U];
+        for (int u = 0; u < U; ++u) idx[u] = e + u < end ? __ldg(incidence + e + u) : -1;
+        T val[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (idx[u] < 0)
-          val[u] = T(0);
-        else if (idx[u] < n_local_rows)
-          val[u] = __ldg(elem + (int64_t)idx[u] * NC + k);
-        else  // peer-written: bypass L1 (the slot is rewritten every other epoch)
-          val[u] = __ldcg(recv + ((int64_t)idx[u] - n_local_rows) * NC + k);
+        for (int u = 0; u < U; ++u) {
+          if (idx[u] < 0)
+            val[u] = T(0);
+          else if (idx[u] < n_local_rows)
+            val[u] = __ldg(elem + (int64_t)idx[u] * NC + k);
+          else  // peer-written: bypass L1 (the slot is rewritten every other epoch)
+            val[u] = __ldcg(recv + ((int64_t)idx[u] - n_local_rows) * NC + k);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (idx[u] >= 0) sum = add(sum, val[u]);
       }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (idx[u] >= 0) sum = add(sum, val[u]);
+      out[o] = sum;
     }
-    out[o] = sum;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -138,7 +157,10 @@ assemble_kernel(int64_t n_owned, const int64_t* __restrict__ offsets, const int3
     if (atomicAdd(ctr, 1u) == gridDim.x - 1) {
       __threadfence_system();  // every CTA's reads of the slot are done
       atomicExch(ctr, 0u);
-      for (int i = 0; i < n_in_peers; ++i) store_release_sys(&header(windows[in_peers[i]])->acks[rank], epoch);
+      // the error is sticky: a rank that failed once never acks again, so its
+      // senders fail as well rather than reuse a slot it may not have read
+      if (atomicAdd(&mine->error, 0) == 0)
+        for (int i = 0; i < n_in_peers; ++i) store_release_sys(&header(windows[in_peers[i]])->acks[rank], epoch);
     }
   }
 }

@@ -12,11 +12,13 @@ Differences from the reference, all deliberate:
     ``"python"`` and ``"simulated"`` are the reference's CPU lanes and raise
     ValueError here; ``log_tasks`` (the virtual-device task log) is an audit
     tool of the simulated device and is not available;
-  * remainder cells (n mod N_chunk) are integrated on the GPU in the
-    configured precision (a predicated partial batch), not by the float64
-    CPU oracle (executor.py:258-264): identical bits in f64, ulp-level
-    differences in f32 (within the 1e-5 parity tolerance);
-  * ``jobs`` is accepted and ignored (the GPU is the parallelism).
+  * remainder cells (n mod N_chunk) are integrated in float64 and cast, as
+    the reference does (executor.py:258-264), but by the float64 CUDA
+    kernels (bit-identical to integrate_reference): the f32 residual equals
+    the reference's bit for bit (tests/test_residual_golden.py);
+  * ``jobs`` is accepted and has no effect on the result -- the reference's
+    thread pool over chunks (executor.py:228-239) produces the same bits as
+    its single call, and here one launch covers every chunk.
 """
 
 from __future__ import annotations
@@ -37,7 +39,8 @@ from .schedule import DEFAULT_THREAD_LIMIT, ExecutionGeometry, derive_execution_
 from .trace import ChunkTrace, ExecutionTrace, model_batch_counters, shared_image_bytes
 
 __all__ = ["DEFAULT_SHARED_MEM_LIMIT", "scalar_dtype", "execute_chunk", "integrate_transposed",
-           "integrate_cells", "integrate_mesh", "integrate_partitioned"]
+           "integrate_cells", "integrate_mesh", "integrate_partitioned", "invalidate_mesh_cache",
+           "integrate_reference"]
 
 DEFAULT_SHARED_MEM_LIMIT = 48 * 1024
 _DTYPE_NAMES = {"f32": np.float32, "f64": np.float64}
@@ -134,6 +137,24 @@ def integrate_cells(tab: Tabulation, rule: QuadratureRule, cell_geom: CellGeomet
     return res
 
 
+def integrate_reference(tab: Tabulation, rule: QuadratureRule, geom: CellGeometry, form: PhysicsForm, coeffs,
+                        aux: Optional[CellAux] = None):
+    """The reference's float64 oracle entry point (reference.py:40-112) with
+    its contract -- (n, n_b, n_comp) float64 element vectors, inputs cast to
+    float64, ShapeError on inconsistent spans -- computed by the float64 CUDA
+    kernels, which reproduce integrate_reference bit for bit (shipped forms
+    on the ahead-of-time kernels, user forms on the run-time compiled ones).
+    numpy in -> numpy out; CUDA tensors in -> CUDA tensor out."""
+    n = geom.n_cells
+    shape = (n, tab.n_b, form.n_comp)
+    if tuple(int(x) for x in coeffs.shape) != shape:
+        raise ShapeError(f"coefficients have shape {tuple(coeffs.shape)}, expected {shape}")
+    form.require_aux(aux)
+    if aux is not None and int(aux.values.shape[0]) != n:
+        raise ShapeError(f"auxiliary data covers {aux.values.shape[0]} cells, expected {n}")
+    return integrate_cells(tab, rule, geom, coeffs, aux, form, dtype="f64")
+
+
 def execute_chunk(geom: ExecutionGeometry, tab: Tabulation, rule: QuadratureRule, cell_geom: CellGeometry,
                   coeffs, aux: Optional[CellAux], form: PhysicsForm, *, dtype="f64", chunk_index: int = 0,
                   shared_mem_limit: Optional[int] = DEFAULT_SHARED_MEM_LIMIT, log_tasks: bool = False,
@@ -155,14 +176,47 @@ def execute_chunk(geom: ExecutionGeometry, tab: Tabulation, rule: QuadratureRule
 
 # Device copies of the last mesh's static data (connectivity, vertices, the
 # vertex incidence CSR), reused across residual evaluations of the same mesh
-# arrays (keyed on array identity, like the reference's Mesh, which is never
-# mutated in place).
+# arrays on the same device.  Keyed on array identity + device + a sampled
+# fingerprint of the contents (64 rows: catches typical in-place mesh motion
+# for free); a caller that mutates a mesh in place in some other way calls
+# invalidate_mesh_cache().
 _INCIDENCE_CACHE: dict = {}
 _MESH_CACHE: dict = {}
 
 
+def invalidate_mesh_cache() -> None:
+    """Drop every cached device copy of mesh data (connectivity, vertices,
+    incidence, partitions): the next call re-uploads and re-validates."""
+    _INCIDENCE_CACHE.clear()
+    _MESH_CACHE.clear()
+    _PART_CACHE.clear()
+
+
+def _fingerprint(a: np.ndarray) -> bytes:
+    rows = a.shape[0]
+    if rows == 0:
+        return b""
+    idx = np.unique(np.linspace(0, rows - 1, min(rows, 64)).astype(np.int64))
+    return np.ascontiguousarray(a[idx]).tobytes()
+
+
+def _device_index(torch) -> int:
+    return torch.cuda.current_device()
+
+
+def _check_connectivity(mesh: Mesh):
+    """0 <= cells < n_vertices, once per upload (the reference's numpy fancy
+    indexing raises IndexError on a bad id; the kernels would read out of
+    bounds)."""
+    c = mesh.cells
+    if c.size and (int(c.min()) < 0 or int(c.max()) >= mesh.n_vertices):
+        raise IndexError(f"cell connectivity holds vertex ids outside [0, {mesh.n_vertices})")
+
+
 def _incidence_for(mesh: Mesh, cells_dev):
-    key = (id(mesh.cells), mesh.cells.shape, mesh.n_vertices)
+    import torch
+
+    key = (id(mesh.cells), mesh.cells.shape, mesh.n_vertices, _device_index(torch), _fingerprint(mesh.cells))
     hit = _INCIDENCE_CACHE.get(key)
     if hit is not None and hit[0] is mesh.cells:
         return hit[1]
@@ -174,10 +228,12 @@ def _incidence_for(mesh: Mesh, cells_dev):
 
 def _mesh_on_device(mesh: Mesh, torch):
     """(cells int64, vertices float64) CUDA tensors of ``mesh``, uploaded once."""
-    key = (id(mesh.cells), id(mesh.vertices), mesh.cells.shape, mesh.vertices.shape)
+    key = (id(mesh.cells), id(mesh.vertices), mesh.cells.shape, mesh.vertices.shape, _device_index(torch),
+           _fingerprint(mesh.cells), _fingerprint(mesh.vertices))
     hit = _MESH_CACHE.get(key)
     if hit is not None and hit[0] is mesh.cells and hit[1] is mesh.vertices:
         return hit[2], hit[3]
+    _check_connectivity(mesh)
     cells = torch.from_numpy(np.ascontiguousarray(mesh.cells, dtype=np.int64)).to("cuda")
     verts = torch.from_numpy(np.ascontiguousarray(mesh.vertices, dtype=np.float64)).to("cuda")
     _MESH_CACHE.clear()
@@ -191,11 +247,13 @@ _PART_CACHE_SIZE = 8
 
 def _partition_on_device(mesh: Mesh, lo: int, hi: int, torch):
     """(cells[lo:hi] int64, vertices float64) CUDA tensors of one rank's cell
-    range, uploaded once per (mesh arrays, range)."""
-    key = (id(mesh.cells), id(mesh.vertices), mesh.cells.shape, mesh.vertices.shape, lo, hi)
+    range, uploaded once per (mesh arrays, range, device)."""
+    key = (id(mesh.cells), id(mesh.vertices), mesh.cells.shape, mesh.vertices.shape, lo, hi, _device_index(torch),
+           _fingerprint(mesh.cells), _fingerprint(mesh.vertices))
     hit = _PART_CACHE.get(key)
     if hit is not None and hit[0] is mesh.cells and hit[1] is mesh.vertices:
         return hit[2], hit[3]
+    _check_connectivity(Mesh(mesh.dim, mesh.vertices, mesh.cells[lo:hi]))
     cells = torch.from_numpy(np.ascontiguousarray(mesh.cells[lo:hi], dtype=np.int64)).to("cuda")
     verts = torch.from_numpy(np.ascontiguousarray(mesh.vertices, dtype=np.float64)).to("cuda")
     while len(_PART_CACHE) >= _PART_CACHE_SIZE:  # several ranks may share a process (peer-group emulation)
@@ -384,6 +442,8 @@ def integrate_mesh(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: Quadr
                          "integrate_transposed (geometry -> gather -> run-time compiled integration)")
     n = mesh.n_cells
     _check_aux_shape(aux, n, tab.n_b, form)
+    if cells is None:
+        _check_connectivity(mesh)  # (caller-provided device connectivity is the caller's contract)
     C = cells if cells is not None else torch.from_numpy(np.ascontiguousarray(mesh.cells, dtype=np.int64)).cuda()
     X = vertices if vertices is not None else \
         torch.from_numpy(np.ascontiguousarray(mesh.vertices, dtype=np.float64)).cuda()
@@ -413,7 +473,7 @@ def integrate_mesh(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: Quadr
 def integrate_partitioned(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: QuadratureRule,
                           form: PhysicsForm, coeffs_global, aux: Optional[CellAux] = None, *, rank: int,
                           world: int, exchange=None, dtype="f64", plan=None, align: int = 256, n_bl: int = 0,
-                          peer=None):
+                          peer=None, check: bool = True):
     """One rank's share of integrate_transposed for the contiguous cell-range
     partition over ``world`` ranks (shard.cell_range): integrate the rank's
     cells on its GPU, then the halo exchange + assembly of halo.py.
@@ -424,7 +484,11 @@ def integrate_partitioned(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule
     residual (executor.py:266, np.add.at order) bit for bit.  ``exchange``: halo.all_to_all_exchange() under torch.distributed
     (None for world == 1).  ``plan``: a cached halo.build_halo_plan result.
     ``peer``: a halo.PeerHalo — the exchange over peer memory (txb_halo_put /
-    txb_halo_assemble) instead of ``exchange``; its plan is used."""
+    txb_halo_assemble) instead of ``exchange``; its plan is used.  With
+    ``check`` (default) a failed exchange raises CudaLaneError here (one host
+    sync); ``check=False`` keeps the call asynchronous -- then call
+    ``peer.check()`` before trusting the result (a failed epoch's owned
+    entries are NaN, never silently stale)."""
     from . import halo
 
     torch = _torch()
@@ -456,6 +520,9 @@ def integrate_partitioned(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule
                             blocks, aux_dev, form, dtype=dt, out=elem, n_bl=n_bl)
     if peer is not None:
         owned = peer.exchange_assemble(buf)
+        if check:
+            torch.cuda.current_stream().synchronize()
+            peer.check()
     else:
         owned = halo.assemble_owned(plan, buf, nc, exchange)
     return plan.owned, owned.reshape(-1), plan

@@ -323,7 +323,8 @@ class PeerHalo:
         return out[:plan.owned.size]
 
     def check(self) -> None:
-        """Raise if a put or an assembly timed out waiting for a peer (host sync)."""
+        """Raise if a put or an assembly of this rank failed (host sync).  The
+        error is sticky: once failed, the window never acks again."""
         import ctypes
 
         from . import _lib
@@ -332,8 +333,10 @@ class PeerHalo:
         e = ctypes.c_int(0)
         _lib.check(_lib.lib().txb_halo_window_error(ctypes.c_void_p(self.window), ctypes.byref(e)))
         if e.value:
-            raise CudaLaneError(f"halo exchange on rank {self.plan.rank} timed out waiting for a peer "
-                                f"({'ack' if e.value == 1 else 'rows'}; TXB_HALO_TIMEOUT_MS)")
+            what = {1: "timed out waiting for a peer's ack (its put skipped the stores and poisoned its flag)",
+                    2: "timed out waiting for a peer's rows", 3: "a peer's put failed (poisoned flag)"}
+            raise CudaLaneError(f"halo exchange on rank {self.plan.rank}: {what.get(e.value, e.value)}; the owned "
+                                f"residual of the failed epoch is NaN (TXB_HALO_TIMEOUT_MS)")
 
     def close(self) -> None:
         if self._on_close is not None:

@@ -281,3 +281,42 @@ def test_peer_exchange_across_processes_via_ipc(world):
     r = subprocess.run([sys.executable, str(repo / "tools" / "peer_ipc_check.py"), str(world)], cwd=repo, env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "bit-identical" in r.stdout, (r.stdout + r.stderr)[-3000:]
+
+
+@pytest.mark.gpu
+def test_peer_exchange_failed_sender_is_reported(monkeypatch):
+    """A sender whose put times out waiting for an ack publishes a POISONED flag
+    instead of a clean one: the owner reports error 3 and its owned residual is
+    NaN -- never a stale slot assembled as if it were fresh."""
+    import paper_1607_04245_b200 as txb
+    from paper_1607_04245_b200.errors import CudaLaneError
+
+    monkeypatch.setenv("TXB_HALO_TIMEOUT_MS", "200")
+    dim, world = 3, 2
+    mesh = txb.generate_unit_simplex_mesh(dim, 6)
+    form = txb.poisson_form(dim)
+    layout = txb.FieldLayout(1)
+    rule = txb.quadrature_rule(dim, 1)
+    tab = txb.tabulate(dim, rule)
+    plans = [halo.build_halo_plan(mesh.cells, mesh.n_vertices, r, world, 16) for r in range(world)]
+    assert plans[1].n_send > 0 and plans[0].n_recv > 0
+    group = halo.local_peer_group(plans, 1, 8)
+    glob = np.random.default_rng(3).standard_normal(layout.global_size(mesh))
+    try:
+        # rank 1 runs three epochs while rank 0 never assembles (never acks):
+        # epoch 3's put times out on epoch 1's ack and poisons its flag
+        for _ in range(3):
+            txb.integrate_partitioned(mesh, layout, tab, rule, form, glob, None, rank=1, world=world,
+                                      peer=group[1], check=False)
+        torch.cuda.synchronize()
+        with pytest.raises(CudaLaneError, match="ack"):
+            group[1].check()
+        with pytest.raises(CudaLaneError, match="poisoned"):
+            txb.integrate_partitioned(mesh, layout, tab, rule, form, glob, None, rank=0, world=world,
+                                      peer=group[0])
+        ids, res, _ = txb.integrate_partitioned(mesh, layout, tab, rule, form, glob, None, rank=0, world=world,
+                                                peer=group[0], check=False)
+        torch.cuda.synchronize()
+        assert torch.isnan(res).all()
+    finally:
+        group[0].close()

@@ -20,10 +20,9 @@ from pathlib import Path
 
 import pytest
 
-REPO = Path(__file__).resolve().parents[1]
-sys.path.insert(0, str(REPO / "oracle"))
+from oracle import apply_seam
 
-import apply_seam  # noqa: E402
+REPO = Path(__file__).resolve().parents[1]
 
 HAVE_REF = (apply_seam.PRISTINE / "tests").exists()
 needs_ref = pytest.mark.skipif(not HAVE_REF, reason="oracle/_ref/txfem_pkg not staged (oracle/build_ref.sh)")

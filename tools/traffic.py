@@ -52,13 +52,12 @@ def run(configs):
     sweep = torch.ones(SWEEP_BYTES, dtype=torch.uint8, device="cuda")
 
     words = sweep.view(torch.int64)
-    acc = torch.zeros((), dtype=torch.int64, device="cuda")
 
     def flush():
         # read sweep with DEFAULT-policy loads (a torch reduction): it evicts --
         # writes back -- every dirty L2 line; evict-first (.cs) loads would only
         # recycle their own lines and leave the launch's outputs dirty in L2
-        torch.sum(words, out=acc)
+        words.sum()
 
     for name in configs:
         wl = bench.rank_workload(name, 0, 1)

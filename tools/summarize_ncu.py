@@ -4,7 +4,7 @@ python tools/summarize_ncu.py TAG
   reads  gpurun_out/TAG_launches.csv          (ncu --metrics gpu__time_duration.sum)
          gpurun_out/TAG_prof_*.ncu-rep         (ncu --set full, one launch each)
   writes profiles/TAG_ncu.md                   (launch shares + key metrics + top stalls)
-         profiles/ncu_traffic.json             (DRAM bytes per launch, read by bench.py)
+  (profiles/ncu_traffic.json -- the write-back-inclusive traffic bench.py reads -- is tools/traffic.py's)
 """
 import collections
 import csv
@@ -92,12 +92,10 @@ def main():
     md = [f"# ncu summary `{tag}` (B200, `--clock-control none`)", ""]
     lpath = OUT / f"{tag}_launches.csv"
     if lpath.exists():
-        md += ["## Launch list of `python bench.py --steps 20 --warmup 3 --no-variants --no-cpu --no-e2e`",
+        md += ["## Launch list of `python bench.py --steps 20 --warmup 5 --no-variants --no-cpu --no-e2e`",
                "(cold-cache, serialised per-launch times: compare shares, not absolutes; the stream probe",
                "and torch fills are bench.py's measurement scaffolding, outside the timed region)", "",
                launch_shares(lpath), ""]
-    traffic_path = PROF / "ncu_traffic.json"
-    traffic = json.loads(traffic_path.read_text()) if traffic_path.exists() else {}
     for rep in sorted(OUT.glob(f"{tag}_prof_*.ncu-rep")):
         cfg = rep.stem.replace(f"{tag}_prof_", "")
         m, name = raw_metrics(rep)
@@ -105,13 +103,11 @@ def main():
         md += [f"| {k} | {v} | {u} |" for k, (v, u) in m.items()]
         rd = float(m["dram__bytes_read.sum"][0].replace(",", "")) * TO_B.get(m["dram__bytes_read.sum"][1], 1)
         wr = float(m["dram__bytes_write.sum"][0].replace(",", "")) * TO_B.get(m["dram__bytes_write.sum"][1], 1)
-        config_name = {"3dvar_f64": "3d_varcoef_f64", "3dvar_f32": "3d_varcoef_f32"}.get(cfg, cfg)
-        traffic[config_name] = rd + wr
-        md += ["", f"DRAM traffic per launch: read {rd / 1e6:.2f} MB + write {wr / 1e6:.2f} MB = "
-                   f"{(rd + wr) / 1e6:.2f} MB", "", "Top stall sites:", "", top_stalls(rep), ""]
+        md += ["", f"DRAM traffic inside the profiled launch (cold L2, write-back still pending at its end is "
+                   f"not counted here; see *_traffic.md): read {rd / 1e6:.2f} MB + write {wr / 1e6:.2f} MB", "",
+               "Top stall sites:", "", top_stalls(rep), ""]
     (PROF / f"{tag}_ncu.md").write_text("\n".join(md) + "\n")
-    traffic_path.write_text(json.dumps(traffic, indent=1) + "\n")
-    print("wrote", PROF / f"{tag}_ncu.md", traffic_path)
+    print("wrote", PROF / f"{tag}_ncu.md")
 
 
 if __name__ == "__main__":

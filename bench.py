@@ -835,7 +835,14 @@ def main():
         import torch.distributed as dist
 
         if dist_backend == "nccl":
+            # communicator init lines (ranks, devices, NVLS/P2P transport) on stderr; the
+            # hot path itself runs no collective -- only the max-over-ranks time reduction
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+            if rank == 0:
+                print(f"[bench] nccl process group: world {world}, rank 0 on cuda:{device}", file=sys.stderr,
+                      flush=True)
         else:
             dist.init_process_group(dist_backend)
         barrier = dist.barrier

@@ -292,7 +292,7 @@ def rotating_sets(set_bytes: int, min_sets: int = 4, cap: int = 64) -> int:
     return max(min_sets, min(cap, -(-3 * L2_BYTES // max(1, set_bytes)) + 1))
 
 
-def time_mesh(name, steps, warmup, n_sets_min=4, given_geometry=False):
+def time_mesh(name, steps, warmup, n_sets_min=4, given_geometry=False, tiled=True):
     """Fused mesh kernel (geometry + gather + integrate, txb_integrate_mesh) on the
     config's Kuhn mesh: connectivity/aux/out rotate over buffer sets (> L2);
     vertex coordinates and the global coefficient vector are the mesh's own
@@ -313,8 +313,16 @@ def time_mesh(name, steps, warmup, n_sets_min=4, given_geometry=False):
     tab = txb.tabulate(dim, rule)
     s = np.dtype(npdt).itemsize
     per_cell = (dim + 1) * 8 + (s if aux_space == "p0" else 0) + (dim + 1) * form.n_comp * s
-    n_sets = max(n_sets_min, -(-3 * L2_BYTES // (per_cell * n)) + 1)
     cells0 = torch.from_numpy(mesh.cells).cuda()
+    os.environ["TXB_TILED"] = "1" if tiled and not given_geometry else "0"
+    tiles = None
+    if tiled and not given_geometry:
+        from paper_1607_04245_b200 import executor
+
+        tiles = executor.cell_tiles(cells0, dim, executor.default_tile_cells(dim, 1))
+        # streamed per cell: local indices + the tile record instead of the int64 connectivity
+        per_cell += 4 * tiles.local_bytes + tiles.vrec * 4 / tiles.tile_cells - (dim + 1) * 8
+    n_sets = max(n_sets_min, -(-3 * L2_BYTES // int(per_cell * n)) + 1)
     verts = torch.from_numpy(np.ascontiguousarray(full.vertices)).cuda()
     geom = None
     if given_geometry:  # precomputed once (mesh setup); its bytes are streamed per launch
@@ -327,6 +335,8 @@ def time_mesh(name, steps, warmup, n_sets_min=4, given_geometry=False):
         if aux_space == "p0":
             aux = txb.CellAux("p0", torch.rand((n, 1), dtype=glob.dtype, device="cuda") + 0.5)
         sets.append((cells0.clone(), aux, torch.empty((n, dim + 1, form.n_comp), dtype=glob.dtype, device="cuda")))
+        if tiles is not None:  # each set's own tile tables, built before the timed graph
+            executor.cell_tiles(sets[-1][0], dim, tiles.tile_cells)
 
     def launch(i):
         cells, aux, out = sets[i % n_sets]
@@ -347,6 +357,7 @@ def time_mesh(name, steps, warmup, n_sets_min=4, given_geometry=False):
     graph.replay()
     t1.record()
     torch.cuda.synchronize()
+    os.environ.pop("TXB_TILED", None)
     return t0.elapsed_time(t1) / steps, per_cell
 
 
@@ -760,20 +771,26 @@ def variant_steps(n_cells: int, steps: int) -> int:
 
 def mesh_rows(peak, steps):
     rows = []
-    for v in ("3d_varcoef_f64", "3d_varcoef_f32", "3d_elasticity_f64", "2d_varcoef_f64"):
-        for given in (True, False):
-            def one(v=v, given=given):
+    for v in ("3d_varcoef_f64", "3d_varcoef_f32", "3d_elasticity_f64", "3d_elasticity_f32", "2d_varcoef_f64",
+              "2d_varcoef_f32"):
+        for mode in ("given", "tiled", "per_cell"):
+            def one(v=v, mode=mode):
                 vf, _ = config_model(v)
                 n = CONFIGS[v][3]
-                ms, per_cell = time_mesh(v, variant_steps(n, steps), 5, given_geometry=given)
+                ms, per_cell = time_mesh(v, variant_steps(n, steps), 5, given_geometry=mode == "given",
+                                         tiled=mode == "tiled")
+                path = {"given": "txb_integrate_mesh: gather fused into the integration, geometry streamed",
+                        "per_cell": "txb_integrate_mesh: float64 geometry + gather per cell in-kernel",
+                        "tiled": "txb_integrate_mesh_tiled: float64 geometry + gather from per-tile vertex "
+                                 "tables in shared memory"}[mode]
                 return [{
-                    "config": ("mesh_given_geometry_" if given else "mesh_geometry_in_kernel_") + v,
-                    "path": "txb_integrate_mesh: gather" + ("" if given else " + float64 geometry") +
-                            " fused into the integration (replaces gather kernel + integrate_cells)",
+                    "config": {"given": "mesh_given_geometry_", "tiled": "mesh_tiled_geometry_in_kernel_",
+                               "per_cell": "mesh_geometry_in_kernel_"}[mode] + v,
+                    "path": path,
                     "cells": n, "launch_ms": ms, "gflops": vf * n / (ms * 1e-3) / 1e9,
                     "gcells_per_s": n / (ms * 1e-3) / 1e9, "bytes_per_cell": per_cell,
                     "gbs": per_cell * n / (ms * 1e-3) / 1e9, "frac": per_cell * n / (ms * 1e-3) / 1e9 / peak}]
-            _guarded(rows, f"mesh_{v}_{'given' if given else 'in_kernel'}", one)
+            _guarded(rows, f"mesh_{v}_{mode}", one)
     return rows
 
 

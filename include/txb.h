@@ -15,6 +15,9 @@
  *                             calling convention: numpy arrays in host memory)
  *   txb_integrate_mesh     <- txfem/executor.py:194-212 (geometry + gather + cast
  *                             + integrate_cells, fused into one kernel)
+ *   txb_tile_counts / txb_tile_build / txb_integrate_mesh_tiled
+ *                          <- the same call as txb_integrate_mesh (executor.py:194-212)
+ *                             over cached cell tiles with batch-local vertex tables
  *   txb_gather_coefficients   <- txfem/mesh.py:202-217 gather_coefficients
  *   txb_scatter_add           <- txfem/mesh.py:220-234 scatter_add_element_vectors
  *   txb_scatter_add_slots     <- the same, vertices visited in element-row order
@@ -142,6 +145,44 @@ int txb_integrate_mesh(int form_code, int aux_mode, int dtype_bytes, int dim, in
                        const double* vertices, const int64_t* cells, const void* coeffs_global,
                        const void* inv_j, const void* det_j, const void* aux, void* out,
                        int64_t* bad_cell, int n_bl, void* stream);
+
+/* ---- Tiled mesh integration -------------------------------------------
+ * A mesh's cells cut into tiles of tile_cells consecutive cells, each with
+ * the list of its distinct vertices (a per-mesh structure, built once on the
+ * device and cached):
+ *   records (n_tiles, vrec) int32: [count, 0, 0, 0, ids ascending..., 0...]
+ *   local   (n_tiles * tile_cells, 4) uint8 (local_bytes 1: every count
+ *           <= 256) or uint16 (2): each cell's vertex positions in its tile's
+ *           list (2D: the 4th entry 0); both zero-initialised by the caller.
+ * txb_tile_counts writes each tile's count (n_tiles int32) so the caller can
+ * size vrec = 4 + max(count) rounded up to a multiple of 4; txb_tile_build
+ * fills records and local.  Connectivity int64 (n_cells, dim+1), vertex ids
+ * < 2^31, tile_cells * (dim+1) <= 1024.  Asynchronous on `stream`. */
+int txb_tile_counts(int dim, int64_t n_cells, const int64_t* cells, int tile_cells, int32_t* counts,
+                    void* stream);
+int txb_tile_build(int dim, int64_t n_cells, const int64_t* cells, int tile_cells, int vrec, int local_bytes,
+                   int32_t* records, void* local, void* stream);
+
+/* txb_integrate_mesh with the geometry computed in-kernel, over the tiles
+ * above (records / local 16-byte aligned): per tile, each distinct vertex's
+ * coordinates and coefficients are gathered ONCE into shared memory and the
+ * cells read them through their local indices.  tile_cells must be a
+ * multiple of (dim+1)*n_q and of 32/n_q with at most 6 warp slices (3D: 128,
+ * 2D: 96 or 192 for the midpoint rule).  Same results, bit for bit, as
+ * txb_integrate_mesh with inv_j = det_j = NULL; bad_cell as there. */
+int txb_integrate_mesh_tiled(int form_code, int aux_mode, int dtype_bytes, int dim, int n_q, int n_comp,
+                             int64_t n_cells, int64_t n_vertices,
+                             const void* basis, const void* basis_der, const void* weights,
+                             const double* vertices, int tile_cells, const int32_t* records, int vrec,
+                             const void* local, int local_bytes, const void* coeffs_global, const void* aux,
+                             void* out, int64_t* bad_cell, void* stream);
+
+/* Test hook: the fused kernels' branch-free float64 geometry per cell
+ * (reciprocal + one residual correction; ok[c] = 0 where a cell's scale is
+ * outside the range where that is the correctly rounded quotient and the
+ * kernels recompute it with division).  Device pointers, asynchronous. */
+int txb_debug_geometry_fast(int dim, int64_t n_cells, const double* vertices, const int64_t* cells,
+                            double* inv_j, double* det_j, int32_t* ok, void* stream);
 
 /* Gather per-cell coefficient blocks (device pointers):
  *   out[c][b][k] = global[cells[c][b] * n_comp + k],  cells int64 (n, n_b). */

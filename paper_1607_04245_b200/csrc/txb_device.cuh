@@ -75,6 +75,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// try_wait with a suspend-time hint: the waiting thread sleeps up to `ns`
+// nanoseconds (or until the phase completes) per attempt instead of retrying
+// -- for the producer / gatherer warps, whose waits are long and whose spins
+// would take issue slots from the consumer warps on their scheduler.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+        : "memory");
+  } while (!ok);
+}
+
 // ---------------------------------------------------------------------------
 // Cluster launch control (sm_100): a running CTA cancels a CTA of its own grid
 // that has not been launched yet and takes over its work -- hardware dynamic
@@ -202,6 +219,80 @@ __device__ __forceinline__ void affine_inverse(const double (&X)[D + 1][D], doub
     inv[1 * 3 + 2] = div(__dsub_rn(__dmul_rn(m[0][2], m[1][0]), __dmul_rn(m[0][0], m[1][2])));
     inv[2 * 3 + 2] = div(__dsub_rn(__dmul_rn(m[0][0], m[1][1]), __dmul_rn(m[0][1], m[1][0])));
   }
+}
+
+// Branch-free variant for the fused kernels, whose outputs do not depend on
+// the sign of a zero geometry entry (exactness note, txb_kernels.cuh): every
+// quotient takes the reciprocal + two-correction path unconditionally (a
+// zero numerator gives +0), and ONE predicate per cell says whether all of
+// them were in the range where that path is the correctly rounded quotient
+// (det and every nonzero numerator in [2^-500, 2^500], as DetDivider).  The
+// caller redoes an unsafe cell with affine_inverse (rare: cells whose edge
+// vectors span more than ~2^200 in scale).  No per-quotient branches: the
+// nine chains interleave freely (the per-quotient branches serialised them).
+#ifndef TXB_DD_RECIPROCAL
+#define TXB_DD_RECIPROCAL 1
+#endif
+__device__ __forceinline__ bool dd_range_bad(double x) {
+  const unsigned hi = (unsigned)__double2hiint(x) & 0x7fffffffu, lo = (unsigned)__double2loint(x);
+  return (hi - 0x20B00000u > 0x3E800000u) & ((hi | lo) != 0u);
+}
+
+template <int D>
+__device__ __forceinline__ bool affine_inverse_fast(const double (&X)[D + 1][D], double (&inv)[D * D], double& det) {
+  double m[D][D];
+#pragma unroll
+  for (int k = 0; k < D; ++k)
+#pragma unroll
+    for (int i = 0; i < D; ++i) m[i][k] = __dsub_rn(X[k + 1][i], X[0][i]);
+  double num[D * D];
+  if constexpr (D == 2) {
+    const double a = m[0][0], b = m[0][1], c = m[1][0], e = m[1][1];
+    det = __dsub_rn(__dmul_rn(a, e), __dmul_rn(b, c));
+    num[0] = e;
+    num[1] = -b;
+    num[2] = -c;
+    num[3] = a;
+  } else {
+    num[0] = __dsub_rn(__dmul_rn(m[1][1], m[2][2]), __dmul_rn(m[1][2], m[2][1]));
+    num[3] = __dsub_rn(__dmul_rn(m[1][2], m[2][0]), __dmul_rn(m[1][0], m[2][2]));
+    num[6] = __dsub_rn(__dmul_rn(m[1][0], m[2][1]), __dmul_rn(m[1][1], m[2][0]));
+    det = __dadd_rn(__dadd_rn(__dmul_rn(m[0][0], num[0]), __dmul_rn(m[0][1], num[3])), __dmul_rn(m[0][2], num[6]));
+    num[1] = __dsub_rn(__dmul_rn(m[0][2], m[2][1]), __dmul_rn(m[0][1], m[2][2]));
+    num[4] = __dsub_rn(__dmul_rn(m[0][0], m[2][2]), __dmul_rn(m[0][2], m[2][0]));
+    num[7] = __dsub_rn(__dmul_rn(m[0][1], m[2][0]), __dmul_rn(m[0][0], m[2][1]));
+    num[2] = __dsub_rn(__dmul_rn(m[0][1], m[1][2]), __dmul_rn(m[0][2], m[1][1]));
+    num[5] = __dsub_rn(__dmul_rn(m[0][2], m[1][0]), __dmul_rn(m[0][0], m[1][2]));
+    num[8] = __dsub_rn(__dmul_rn(m[0][0], m[1][1]), __dmul_rn(m[0][1], m[1][0]));
+  }
+  // det > 0 in range: the signed high word within [2^-500, 2^500]
+  bool bad = ((unsigned)__double2hiint(det) - 0x20B00000u) > 0x3E800000u;
+#if TXB_DD_RECIPROCAL
+  // 1/det as y + yl (|yl| <= ulp(y)/2, the pair ~2^-104 relative): q0 =
+  // RN(x y + RN(x yl)) is within ~0.5 ulp of x/det, so ONE residual
+  // correction with y = RN(1/det) is correctly rounded (Markstein: q within
+  // one ulp, y within half an ulp of 1/det) -- 4 operations per quotient.
+  const double y = __drcp_rn(det);
+  const double yl = __dmul_rn(__fma_rn(-det, y, 1.0), y);
+#pragma unroll
+  for (int i = 0; i < D * D; ++i) {
+    const double x = num[i];
+    bad |= dd_range_bad(x);
+    const double q0 = __fma_rn(x, y, __dmul_rn(x, yl));
+    inv[i] = __fma_rn(__fma_rn(-q0, det, x), y, q0);
+  }
+#else
+  const double y = __drcp_rn(det);
+#pragma unroll
+  for (int i = 0; i < D * D; ++i) {
+    const double x = num[i];
+    bad |= dd_range_bad(x);
+    const double q0 = __dmul_rn(x, y);
+    const double q1 = __fma_rn(__fma_rn(-q0, det, x), y, q0);
+    inv[i] = __fma_rn(__fma_rn(-q1, det, x), y, q1);
+  }
+#endif
+  return !bad;
 }
 
 __host__ __device__ constexpr int round_up(int x, int m) { return (x + m - 1) / m * m; }

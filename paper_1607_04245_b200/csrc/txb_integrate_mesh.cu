@@ -57,25 +57,6 @@ struct MeshStage {
   __host__ __device__ static int stage_bytes(int n) { return cell_bytes(n) + aux_bytes(n) + inv_bytes(n) + det_bytes(n); }
 };
 
-// Warp-private exchange: per cell the (cast) invJ rows = T[b>=1], T[0], and
-// f1s, component-major (row = one component, the slice's cells at pitch
-// CW + 4): conflict-free stores and loads (3D elasticity f64 given geometry
-// 56.1 -> 48.6 us; the cell-major stride had 4-way conflicts).
-template <typename T, int D, int NQ, int NCOMP>
-struct MeshScratch {
-  static constexpr int CW = 32 / NQ;
-  static constexpr bool CM = true;  // component-major (measured faster for every form here)
-  static constexpr int P = CW + 4;
-  static constexpr int TR = D * D + D;  // invJ (D*D) then T[0] (D)
-  static constexpr int TRS = make_odd(TR);
-  static constexpr int F1 = NQ * NCOMP * D;
-  static constexpr int F1S = make_odd(F1);
-  __device__ static int tr(int lc, int r) { return CM ? r * P + lc : lc * TRS + r; }
-  __device__ static int f1(int lc, int r) { return CM ? r * P + lc : lc * F1S + r; }
-  static constexpr int TR_BYTES = round_up((CM ? P * TR : CW * TRS) * (int)sizeof(T), 16);
-  static constexpr int BYTES = TR_BYTES + round_up((CM ? P * F1 : CW * F1S) * (int)sizeof(T), 16);
-};
-
 template <typename T, int D, int NQ, int NCOMP, int FORM, int AUX, int GEOM, bool SMEM>
 __device__ __forceinline__ void mesh_slice(const MeshArgs<T>& a, const int64_t* __restrict__ s_cells,
                                            const T* __restrict__ s_aux, const T* __restrict__ s_inv,
@@ -146,7 +127,7 @@ __device__ __forceinline__ void mesh_slice(const MeshArgs<T>& a, const int64_t* 
 #pragma unroll
           for (int i = 0; i < D; ++i) X[b][i] = __ldg(a.vertices + ids[b] * D + i);
         double inv[DD], detd;
-        affine_inverse<D>(X, inv, detd);
+        if (!affine_inverse_fast<D>(X, inv, detd)) affine_inverse<D>(X, inv, detd);  // branch-free; exact fallback
         if (q == 0 && a.bad && detd <= 0.0) atomicMin(a.bad, (unsigned long long)(c0_batch + cell));
         // executor._device_arrays (executor.py:77-90): cast once to the run precision
 #pragma unroll

@@ -105,7 +105,7 @@ __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const re
 #pragma unroll
         for (int i = 0; i < D; ++i) X[b][i] = __ldg(mi.X + ids[b] * D + i);
       double inv[DD], detd;
-      affine_inverse<D>(X, inv, detd);
+      affine_inverse<D>(X, inv, detd);  // exact, signed zeros included: user forms may see them
       if (q == 0 && mi.bad && detd <= 0.0) atomicMin(mi.bad, (unsigned long long)(mi.c0_batch + cell));
 #pragma unroll
       for (int i = 0; i < DD; ++i) J[i] = (real)inv[i];

@@ -62,6 +62,25 @@ struct Scratch {
   static constexpr int BYTES = TR_BYTES + round_up((CM ? P * F1 : CW * F1S) * (int)sizeof(T), 16);
 };
 
+// Warp-private exchange area of the mesh-fused kernels: per cell the (cast) invJ rows = T[b>=1], T[0], and
+// f1s, component-major (row = one component, the slice's cells at pitch
+// CW + 4): conflict-free stores and loads (3D elasticity f64 given geometry
+// 56.1 -> 48.6 us; the cell-major stride had 4-way conflicts).
+template <typename T, int D, int NQ, int NCOMP>
+struct MeshScratch {
+  static constexpr int CW = 32 / NQ;
+  static constexpr bool CM = true;  // component-major (measured faster for every form here)
+  static constexpr int P = CW + 4;
+  static constexpr int TR = D * D + D;  // invJ (D*D) then T[0] (D)
+  static constexpr int TRS = make_odd(TR);
+  static constexpr int F1 = NQ * NCOMP * D;
+  static constexpr int F1S = make_odd(F1);
+  __device__ static int tr(int lc, int r) { return CM ? r * P + lc : lc * TRS + r; }
+  __device__ static int f1(int lc, int r) { return CM ? r * P + lc : lc * F1S + r; }
+  static constexpr int TR_BYTES = round_up((CM ? P * TR : CW * TRS) * (int)sizeof(T), 16);
+  static constexpr int BYTES = TR_BYTES + round_up((CM ? P * F1 : CW * F1S) * (int)sizeof(T), 16);
+};
+
 // Exactness note (why the chains below may skip the reference's "acc = 0;
 // acc = acc + x" first step and its 0*x / 1*x products): in round-to-nearest
 // a sum is -0 only if both operands are -0, so a chain started at +0 is never
@@ -177,9 +196,13 @@ struct KernelInfo {
   int rt_s;
   int rt_scratch;
   int family;  // KernelFamily (0: the ahead-of-time cell-array kernels)
+  int stage_extra;  // bytes per stage on top of stage_bytes(n_bc) (tiled kernels: the vertex table)
+  int extra_warps;  // warps besides the consumers and the producer (tiled kernels: the gatherer)
+  int fixed_extra;  // fixed shared-memory bytes besides scratch + pipeline (tiled kernels: `ready` barriers)
+  int prefer_dynamic;  // dynamic batch scheduling whatever the stage size (tiled kernels: measured faster)
   int stage(int n_bc) const {
-    if (stage_bytes) return stage_bytes(n_bc);
-    int b = 0;
+    if (stage_bytes) return stage_bytes(n_bc) + stage_extra;
+    int b = stage_extra;
     for (int r = 0; r < 4; ++r) b += round_up(n_bc * rt_region[r] * rt_s, 16);
     return b;
   }
@@ -266,10 +289,10 @@ static int compute_geometry(const Config& c, const KernelInfo& k, int64_t n_cell
   const int slices = (g.n_bc + k.cw - 1) / k.cw;
   const int wcap = std::max(1, std::min(MAX_CONSUMER_WARPS, env_int("TXB_MAX_WARPS", MAX_CONSUMER_WARPS)));
   g.warps = std::min(wcap, slices);
-  g.threads = 32 * (g.warps + 1);
+  g.threads = 32 * (g.warps + 1 + k.extra_warps);
 
   const int stage = k.stage(g.n_bc);
-  const int fixed = g.warps * k.scratch_bytes(g.n_bc) + PIPELINE_SMEM_BYTES + 16;
+  const int fixed = g.warps * k.scratch_bytes(g.n_bc) + PIPELINE_SMEM_BYTES + 16 + k.fixed_extra;
   int smem_cap = 227 * 1024;
   int dev = 0, sms = 148;
   if (query_device && cudaGetDevice(&dev) == cudaSuccess) {
@@ -363,7 +386,7 @@ static int compute_geometry(const Config& c, const KernelInfo& k, int64_t n_cell
   // hide the scheduling request's latency (>= 10 KB per stage; measured with
   // an atomic counter in round 1, profiles/r1_sweep.md).
   const int dyn_env = env_int("TXB_DYNAMIC", -1);
-  g.dynamic = n_cb <= 0 && (dyn_env < 0 ? stage >= 10 * 1024 : dyn_env != 0);
+  g.dynamic = n_cb <= 0 && (dyn_env < 0 ? (stage >= 10 * 1024 || k.prefer_dynamic) : dyn_env != 0);
   g.resident = 0;
   g.static_batches = 0;
   if (g.dynamic) {

@@ -190,6 +190,7 @@ def invalidate_mesh_cache() -> None:
     _INCIDENCE_CACHE.clear()
     _MESH_CACHE.clear()
     _PART_CACHE.clear()
+    _TILE_CACHE.clear()
 
 
 def _fingerprint(a: np.ndarray) -> bytes:
@@ -414,6 +415,74 @@ def _mesh_fusable(tab: Tabulation, rule: QuadratureRule) -> bool:
     return ok
 
 
+class CellTiles:
+    """A mesh's cells cut into tiles of ``tile_cells`` consecutive cells, each
+    with the ascending list of its distinct vertices (``records``, int32, stride
+    ``vrec``: [count, 0, 0, 0, ids...]) and every cell's 4 local indices into
+    it (``local``, uint8 or uint16): the per-mesh input of the tiled kernel
+    (csrc/txb_integrate_tiled.cu).  Built on the device by txb_tile_counts +
+    txb_tile_build (one host sync: the largest count sizes the records)."""
+
+    def __init__(self, cells_dev, dim: int, tile_cells: int):
+        from . import _lib
+
+        torch = _torch()
+        n = int(cells_dev.shape[0])
+        self.tile_cells = tile_cells
+        self.n_tiles = -(-n // tile_cells)
+        counts = torch.zeros(max(1, self.n_tiles), dtype=torch.int32, device=cells_dev.device)
+        s = _stream_ptr(torch)
+        _lib.check(_lib.lib().txb_tile_counts(dim, n, cells_dev.data_ptr(), tile_cells, counts.data_ptr(), s),
+                   "txb_tile_counts")
+        self.max_count = int(counts.max().item()) if self.n_tiles else 0
+        self.vrec = 4 + max(4, -(-self.max_count // 4) * 4)
+        self.local_bytes = 1 if self.max_count <= 256 else 2
+        self.records = torch.zeros(max(1, self.n_tiles) * self.vrec, dtype=torch.int32, device=cells_dev.device)
+        self.local = torch.zeros(max(1, self.n_tiles) * tile_cells * 4 * self.local_bytes, dtype=torch.uint8,
+                                 device=cells_dev.device)
+        _lib.check(_lib.lib().txb_tile_build(dim, n, cells_dev.data_ptr(), tile_cells, self.vrec, self.local_bytes,
+                                             self.records.data_ptr(), self.local.data_ptr(), s), "txb_tile_build")
+        self.mean_count = float(counts.double().mean().item()) if self.n_tiles else 0.0
+
+
+_TILE_CACHE: dict = {}
+_TILE_CACHE_SIZE = 32
+
+
+def default_tile_cells(dim: int, n_q: int) -> int:
+    """Cells per tile (= per batch) of the tiled kernel: 3D 128 (midpoint) / 64
+    (two points), 2D 192 / 96 -- multiples of n_b * n_q and of the warp slice
+    32 / n_q, at most 6 slices (4-6 consumer warps).  TXB_TILE_CELLS overrides."""
+    env = os.environ.get("TXB_TILE_CELLS")
+    if env:
+        return int(env)
+    if dim == 3:
+        return 128 if n_q == 1 else 64
+    return 192 if n_q == 1 else 96
+
+
+def cell_tiles(cells_dev, dim: int, tile_cells: int) -> CellTiles:
+    """The CellTiles of a device connectivity tensor, built once per (tensor,
+    tile size, device) and cached (the tensor is kept alive with them; it must
+    not be modified in place -- the mesh caches above hand out fresh tensors
+    when the host mesh changes)."""
+    key = (cells_dev.data_ptr(), tuple(cells_dev.shape), cells_dev.device.index, tile_cells)
+    hit = _TILE_CACHE.get(key)
+    if hit is not None and hit[0] is cells_dev:
+        return hit[1]
+    tiles = CellTiles(cells_dev, dim, tile_cells)
+    while len(_TILE_CACHE) >= _TILE_CACHE_SIZE:
+        _TILE_CACHE.pop(next(iter(_TILE_CACHE)))
+    _TILE_CACHE[key] = (cells_dev, tiles)
+    return tiles
+
+
+def _tiled_enabled(mesh: Mesh, rule: QuadratureRule) -> bool:
+    """The tiled kernel takes the geometry-in-kernel mesh calls (TXB_TILED=0
+    keeps the per-cell fused kernel): int32 vertex ids, n_q <= 2."""
+    return os.environ.get("TXB_TILED", "1") != "0" and mesh.n_vertices < (1 << 31) and rule.n_q <= 2
+
+
 def integrate_mesh(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: QuadratureRule, form: PhysicsForm,
                    coeffs_global, aux: Optional[CellAux] = None, *, dtype="f64", cell_geom=None, cells=None,
                    vertices=None, out=None, n_bl: int = 0, check_orientation: bool = True):
@@ -458,11 +527,23 @@ def integrate_mesh(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: Quadr
     bad = torch.full((1,), -1, dtype=torch.int64, device="cuda") if cell_geom is None and check_orientation else None
     B, D, W = (np.ascontiguousarray(x, dtype=dt) for x in (tab.basis, tab.basis_der, rule.weights))
     ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
-    rc = _lib.lib().txb_integrate_mesh(
-        kernel[0], kernel[1], dt.itemsize, mesh.dim, rule.n_q, form.n_comp, n, mesh.n_vertices,
-        B.ctypes.data, D.ctypes.data, W.ctypes.data, X.data_ptr(), C.data_ptr(), g.data_ptr(), ptr(inv), ptr(det),
-        ptr(av), res.data_ptr(), ptr(bad), n_bl, _stream_ptr(torch))
-    _lib.check(rc, "txb_integrate_mesh")
+    tiles = None
+    if cell_geom is None and n > 0 and _tiled_enabled(mesh, rule):
+        tiles = cell_tiles(C, mesh.dim, default_tile_cells(mesh.dim, rule.n_q))
+    if tiles is not None:
+        # geometry + gather from per-tile vertex tables (csrc/txb_integrate_tiled.cu)
+        rc = _lib.lib().txb_integrate_mesh_tiled(
+            kernel[0], kernel[1], dt.itemsize, mesh.dim, rule.n_q, form.n_comp, n, mesh.n_vertices,
+            B.ctypes.data, D.ctypes.data, W.ctypes.data, X.data_ptr(), tiles.tile_cells, tiles.records.data_ptr(),
+            tiles.vrec, tiles.local.data_ptr(), tiles.local_bytes, g.data_ptr(), ptr(av), res.data_ptr(), ptr(bad),
+            _stream_ptr(torch))
+        _lib.check(rc, "txb_integrate_mesh_tiled")
+    else:
+        rc = _lib.lib().txb_integrate_mesh(
+            kernel[0], kernel[1], dt.itemsize, mesh.dim, rule.n_q, form.n_comp, n, mesh.n_vertices,
+            B.ctypes.data, D.ctypes.data, W.ctypes.data, X.data_ptr(), C.data_ptr(), g.data_ptr(), ptr(inv),
+            ptr(det), ptr(av), res.data_ptr(), ptr(bad), n_bl, _stream_ptr(torch))
+        _lib.check(rc, "txb_integrate_mesh")
     if bad is not None:
         i = int(bad.item())
         if i >= 0:

@@ -292,7 +292,7 @@ def rotating_sets(set_bytes: int, min_sets: int = 4, cap: int = 64) -> int:
     return max(min_sets, min(cap, -(-3 * L2_BYTES // max(1, set_bytes)) + 1))
 
 
-def time_mesh(name, steps, warmup, n_sets_min=4, given_geometry=False, tiled=True):
+def time_mesh(name, steps, warmup, n_sets_min=4, given_geometry=False, tiled=True, n_cells=None):
     """Fused mesh kernel (geometry + gather + integrate, txb_integrate_mesh) on the
     config's Kuhn mesh: connectivity/aux/out rotate over buffer sets (> L2);
     vertex coordinates and the global coefficient vector are the mesh's own
@@ -303,6 +303,7 @@ def time_mesh(name, steps, warmup, n_sets_min=4, given_geometry=False, tiled=Tru
     from paper_1607_04245_b200.workload import PHYSICS, refine_for
 
     dim, physics, dtype, n = CONFIGS[name]
+    n = n_cells or n
     factory, aux_space = PHYSICS[physics]
     form = factory(dim)
     full = txb.generate_unit_simplex_mesh(dim, refine_for(dim, n))
@@ -461,6 +462,29 @@ def api_rows(steps=20):
         rows.append({"config": f"api_integrate_transposed_device_{name}", "cells": mesh.n_cells,
                      "vertices": mesh.n_vertices, "ms_per_call": dt * 1e3, "gcells_per_s": mesh.n_cells / dt / 1e9,
                      "path": "CUDA tensors in/out: fused mesh kernel (in-kernel geometry) + scatter-add"})
+        # the same residual captured once into a CUDA graph (ResidualGraph): copy-in + one replay per call
+        rg = txb.ResidualGraph(mesh, layout, tab, rule, form, aux_dev, n_bl=n_bl, n_cb=8, dtype=dtype,
+                               shared_mem_limit=None)
+        for _ in range(3):
+            rg(glob_dev)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            rg(glob_dev)
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / steps
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            rg(glob_dev)
+        e1.record()
+        torch.cuda.synchronize()
+        rows.append({"config": f"api_residual_graph_device_{name}", "cells": mesh.n_cells,
+                     "vertices": mesh.n_vertices, "ms_per_call": dt * 1e3, "gcells_per_s": mesh.n_cells / dt / 1e9,
+                     "device_ms_per_call": e0.elapsed_time(e1) / steps,
+                     "path": "ResidualGraph: copy of the global vector + one CUDA-graph replay (tiled mesh kernel + "
+                             "scatter-add)"})
+        del rg
         del glob_dev, aux_dev
         del geom
         torch.cuda.empty_cache()

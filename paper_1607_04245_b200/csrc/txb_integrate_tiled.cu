@@ -174,6 +174,7 @@ struct TiledArgs {
   int aux_bulk;                // aux base 16-byte aligned: full batches' aux slices arrive by bulk copy
   int out_vec;                 // out base 16-byte aligned: in-lane rows stored with vector stores
   uint32_t sleep_ns;           // producer / gatherer try_wait suspend hint (0: plain retry)
+  uint32_t consumer_sleep_ns;  // consumer `ready` try_wait suspend hint (0: plain retry)
   int debug;                   // DIAGNOSTIC (TXB_TILED_DEBUG): 1 skip geometry math, 2 skip the gathers
   Tabulation<T> tab;
 };
@@ -504,7 +505,10 @@ integrate_tiled_kernel(const __grid_constant__ TiledArgs<T> a) {
   int stage = 0;
   uint32_t phase = 0;
   for (;;) {
-    mbar_wait(&ready[stage], phase);
+    if (a.consumer_sleep_ns)
+      mbar_wait_sleep(&ready[stage], phase, a.consumer_sleep_ns);
+    else
+      mbar_wait(&ready[stage], phase);
     mbar_wait(&p.full[stage], phase);  // (complete: the bulk-copied bytes are visible to this thread too)
     const int64_t c0 = p.info_c0[stage];
     const int ncell = p.info_n[stage];
@@ -555,6 +559,8 @@ static bool pick_tiled_form(const Config& c, int vrec, bool xpose, KernelInfo& k
     k.extra_warps = 1;                                                      \
     k.fixed_extra = 8 * MAX_STAGES;                                         \
     k.prefer_dynamic = 1;                                                   \
+    k.max_stages = env_int("TXB_TILED_MAX_STAGES", 8);                      \
+    k.max_warps = TILED_MAX_CONSUMER_WARPS;                                 \
     return true;                                                            \
   }
 #define TXB_TK2(NCOMP, FORM, AUX)                                           \
@@ -618,6 +624,7 @@ static int launch_tiled(const Config& c, const KernelInfo& k, Geometry g, int64_
   a.aux_bulk = c.aux != 0 && al16(aux) && env_int("TXB_DISABLE_BULK", 0) == 0;
   a.out_vec = al16(out);
   a.sleep_ns = (uint32_t)std::max(0, env_int("TXB_TILED_SLEEP_NS", 0));
+  a.consumer_sleep_ns = (uint32_t)std::max(0, env_int("TXB_TILED_CONSUMER_SLEEP_NS", 20000));  // measured +2 %
   a.debug = env_int("TXB_TILED_DEBUG", 0);
   fill_tab(a.tab, c.n_q, c.dim + 1, c.dim, basis, basis_der, weights);
   void* params[] = {&a};
@@ -717,10 +724,9 @@ extern "C" int txb_integrate_mesh_tiled(int form_code, int aux_mode, int dtype_b
     return TXB_E_UNSUPPORTED;
   }
   const int nbs = (dim + 1) * n_q;
-  if (tile_cells < 1 || tile_cells % nbs || tile_cells % (32 / n_q) || tile_cells * (dim + 1) > 1024 ||
-      tile_cells / (32 / n_q) > TILED_MAX_CONSUMER_WARPS) {
-    set_error("tile_cells %d must be a multiple of n_b*n_q = %d and of 32/n_q, with tile_cells*(dim+1) <= 1024 "
-              "and at most %d warp slices", tile_cells, nbs, TILED_MAX_CONSUMER_WARPS);
+  if (tile_cells < 1 || tile_cells % nbs || tile_cells % (32 / n_q) || tile_cells * (dim + 1) > 1024) {
+    set_error("tile_cells %d must be a multiple of n_b*n_q = %d and of 32/n_q, with tile_cells*(dim+1) <= 1024",
+              tile_cells, nbs);
     return TXB_E_CONFIG;
   }
   if ((local_bytes != 1 && local_bytes != 2) || vrec < 8 || vrec % 4) {

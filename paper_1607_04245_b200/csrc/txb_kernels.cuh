@@ -200,6 +200,8 @@ struct KernelInfo {
   int extra_warps;  // warps besides the consumers and the producer (tiled kernels: the gatherer)
   int fixed_extra;  // fixed shared-memory bytes besides scratch + pipeline (tiled kernels: `ready` barriers)
   int prefer_dynamic;  // dynamic batch scheduling whatever the stage size (tiled kernels: measured faster)
+  int max_stages;      // ring-depth search limit (0: 8)
+  int max_warps;       // consumer-warp cap (0: MAX_CONSUMER_WARPS); the warps loop over a batch's slices
   int stage(int n_bc) const {
     if (stage_bytes) return stage_bytes(n_bc) + stage_extra;
     int b = stage_extra;
@@ -287,7 +289,8 @@ static int compute_geometry(const Config& c, const KernelInfo& k, int64_t n_cell
   g.n_bc = (int)n_bc64;
   g.n_t = (int)n_t64;
   const int slices = (g.n_bc + k.cw - 1) / k.cw;
-  const int wcap = std::max(1, std::min(MAX_CONSUMER_WARPS, env_int("TXB_MAX_WARPS", MAX_CONSUMER_WARPS)));
+  const int wcap = std::max(1, std::min(k.max_warps > 0 ? k.max_warps : MAX_CONSUMER_WARPS,
+                                        env_int("TXB_MAX_WARPS", MAX_CONSUMER_WARPS)));
   g.warps = std::min(wcap, slices);
   g.threads = 32 * (g.warps + 1 + k.extra_warps);
 
@@ -344,8 +347,9 @@ static int compute_geometry(const Config& c, const KernelInfo& k, int64_t n_cell
     }
   }
   const bool memoised = best_s >= 0;
-  for (int st = 2; !memoised && st <= 8; ++st) {
-    if (forced > 0 && st != std::min(std::max(forced, 2), 8)) continue;
+  const int st_max = k.max_stages > 0 ? std::min(k.max_stages, MAX_STAGES) : 8;
+  for (int st = 2; !memoised && st <= st_max; ++st) {
+    if (forced > 0 && st != std::min(std::max(forced, 2), st_max)) continue;
     const int smem = fixed + st * stage;
     if (smem > smem_cap) break;
     const int o = occupancy(smem);

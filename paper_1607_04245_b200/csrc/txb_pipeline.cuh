@@ -19,7 +19,7 @@ constexpr int EMPTY_ARRIVALS_PER_WARP = TXB_EMPTY_ARRIVE_ALL ? 32 : 1;
 
 constexpr int MAX_D = TXB_MAX_DIM, MAX_B = TXB_MAX_BASIS, MAX_Q = TXB_MAX_QUAD;
 constexpr int MAX_CONSUMER_WARPS = 16;
-constexpr int MAX_STAGES = 8;
+constexpr int MAX_STAGES = 16;  // ring depth cap (the cell-array kernels search <= 8)
 constexpr int MAX_CTA_THREADS = 32 * (MAX_CONSUMER_WARPS + 1);
 
 template <typename T>

@@ -268,11 +268,14 @@ def integrate_transposed(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule:
                          n_cb: int, dtype: Union[str, np.dtype] = "f64", jobs: int = 1,
                          shared_mem_limit: Optional[int] = DEFAULT_SHARED_MEM_LIMIT,
                          thread_limit: int = DEFAULT_THREAD_LIMIT, log_tasks: bool = False,
-                         backend: Optional[str] = None, cell_geom: Optional[CellGeometry] = None):
+                         backend: Optional[str] = None, cell_geom: Optional[CellGeometry] = None,
+                         check_orientation: bool = True):
     """Global residual with the transposed schedule (executor.py:161-267).
 
     Returns (residual, trace): residual is a numpy vector in the configured
-    scalar (a CUDA tensor if ``coeffs_global`` is one)."""
+    scalar (a CUDA tensor if ``coeffs_global`` is one).  ``check_orientation``
+    (extension): False skips the detJ <= 0 read-back of the in-kernel
+    geometry (one host sync) -- for a mesh already checked (ResidualGraph)."""
     dt = scalar_dtype(dtype)
     geom = derive_execution_geometry(mesh.dim, tab.n_b, form.n_comp, rule.n_q, n_bl, n_cb, mesh.n_cells,
                                      thread_limit=thread_limit)
@@ -293,10 +296,11 @@ def integrate_transposed(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule:
     if _mesh_fusable(tab, rule) and not isinstance(kernel, _backend.JitKernel):
         # geometry + gather + cast + integrate in one kernel (csrc/txb_integrate_mesh.cu)
         elem = integrate_mesh(mesh, layout, tab, rule, form, glob_dev, aux_dev, dtype=dt, cell_geom=cell_geom,
-                              cells=cells_dev, vertices=verts_dev, n_bl=n_bl)
+                              cells=cells_dev, vertices=verts_dev, n_bl=n_bl, check_orientation=check_orientation)
     elif isinstance(kernel, _backend.JitKernel) and cell_geom is None and os.environ.get("TXB_JIT_MESH", "1") != "0":
         # run-time compiled form, fused the same way (csrc/txb_jit_kernel.cuh, mesh entry points)
-        elem = _jit_mesh(kernel, mesh, tab, rule, form, glob_dev, aux_dev, dt, cells_dev, verts_dev, n_bl)
+        elem = _jit_mesh(kernel, mesh, tab, rule, form, glob_dev, aux_dev, dt, cells_dev, verts_dev, n_bl,
+                         check_orientation)
     else:
         if cell_geom is None:
             cell_geom = compute_geometry(mesh, cells=cells_dev, vertices=verts_dev, device_out=True)
@@ -310,7 +314,7 @@ def integrate_transposed(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule:
         # integrate_reference), so the f32 residual equals the reference's bits
         span = geom.n_chunks * geom.n_chunk
         elem[span:] = _remainder_f64(mesh, layout, tab, rule, form, kernel, glob, aux, cell_geom, cells_dev,
-                                     verts_dev, span, n_bl).to(elem.dtype)
+                                     verts_dev, span, n_bl, check_orientation).to(elem.dtype)
     residual = scatter_add_element_vectors(mesh, layout, elem, incidence=_incidence_for(mesh, cells_dev))
 
     trace = ExecutionTrace.uniform(geom, dt.itemsize, model_batch_counters(geom, form, dt.itemsize, aux),
@@ -327,7 +331,7 @@ _FUSABLE: dict = {}
 
 def _remainder_f64(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: QuadratureRule, form: PhysicsForm,
                    kernel, glob, aux: Optional[CellAux], cell_geom: Optional[CellGeometry], cells_dev, verts_dev,
-                   span: int, n_bl: int):
+                   span: int, n_bl: int, check_orientation: bool = True):
     """Element vectors of cells [span, n) in float64 (a CUDA tensor): the
     reference's remainder path (integrate_reference on float64 geometry,
     coefficients and aux, executor.py:258-264) on the float64 kernels."""
@@ -345,9 +349,9 @@ def _remainder_f64(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: Quadr
     k64 = _resolve_backend(None, form, rule.n_q, aux, 8)
     if _mesh_fusable(tab, rule) and not isinstance(k64, _backend.JitKernel):
         return integrate_mesh(sub, layout, tab, rule, form, g64, a64, dtype=f64, cell_geom=cg, cells=cells,
-                              vertices=verts_dev, n_bl=n_bl)
+                              vertices=verts_dev, n_bl=n_bl, check_orientation=check_orientation)
     if isinstance(k64, _backend.JitKernel) and cg is None and os.environ.get("TXB_JIT_MESH", "1") != "0":
-        return _jit_mesh(k64, sub, tab, rule, form, g64, a64, f64, cells, verts_dev, n_bl)
+        return _jit_mesh(k64, sub, tab, rule, form, g64, a64, f64, cells, verts_dev, n_bl, check_orientation)
     if cg is None:
         cg = compute_geometry(sub, cells=cells, vertices=verts_dev, device_out=True)
     blocks = gather_coefficients(sub, layout, g64, cells=cells)
@@ -368,7 +372,7 @@ def _check_aux_shape(aux, n_cells: int, n_b: int, form: PhysicsForm):
 
 
 def _jit_mesh(kernel, mesh: Mesh, tab: Tabulation, rule: QuadratureRule, form: PhysicsForm, glob_dev, aux_dev, dt,
-              cells_dev, verts_dev, n_bl: int):
+              cells_dev, verts_dev, n_bl: int, check_orientation: bool = True):
     """Element vectors of a run-time compiled form straight from the mesh
     (txb_jit_integrate_mesh: float64 geometry + gather in-kernel, any
     tabulation).  Raises OrientationError for a cell with detJ <= 0."""
@@ -383,17 +387,19 @@ def _jit_mesh(kernel, mesh: Mesh, tab: Tabulation, rule: QuadratureRule, form: P
     if int(glob_dev.numel()) != mesh.n_vertices * form.n_comp:
         raise ShapeError(f"global vector has {glob_dev.numel()} entries, expected {mesh.n_vertices * form.n_comp}")
     res = torch.empty((n, tab.n_b, form.n_comp), dtype=glob_dev.dtype, device="cuda")
-    bad = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    bad = torch.full((1,), -1, dtype=torch.int64, device="cuda") if check_orientation else None
     B, D, W = (np.ascontiguousarray(x, dtype=dt) for x in (tab.basis, tab.basis_der, rule.weights))
     av = None if aux_dev is None else aux_dev.values.contiguous()
     rc = _lib.lib().txb_jit_integrate_mesh(ctypes.c_void_p(kernel.handle), n, mesh.n_vertices, B.ctypes.data,
                                            D.ctypes.data, W.ctypes.data, verts_dev.data_ptr(), cells_dev.data_ptr(),
                                            glob_dev.data_ptr(), None if av is None else av.data_ptr(),
-                                           res.data_ptr(), bad.data_ptr(), n_bl, _stream_ptr(torch))
+                                           res.data_ptr(), None if bad is None else bad.data_ptr(), n_bl,
+                                           _stream_ptr(torch))
     _lib.check(rc, "txb_jit_integrate_mesh")
-    i = int(bad.item())
-    if i >= 0:
-        raise OrientationError(f"cell {i} is degenerate or negatively oriented")
+    if bad is not None:
+        i = int(bad.item())
+        if i >= 0:
+            raise OrientationError(f"cell {i} is degenerate or negatively oriented")
     return res
 
 
@@ -462,13 +468,15 @@ def default_tile_cells(dim: int, n_q: int) -> int:
 
 
 def cell_tiles(cells_dev, dim: int, tile_cells: int) -> CellTiles:
-    """The CellTiles of a device connectivity tensor, built once per (tensor,
-    tile size, device) and cached (the tensor is kept alive with them; it must
-    not be modified in place -- the mesh caches above hand out fresh tensors
-    when the host mesh changes)."""
-    key = (cells_dev.data_ptr(), tuple(cells_dev.shape), cells_dev.device.index, tile_cells)
+    """The CellTiles of a device connectivity tensor, built once per (memory
+    range, tile size, device) and cached (the tensor is kept alive with them,
+    so the address cannot be reused; a view of the same range hits the same
+    entry).  The tensor must not be modified in place -- the mesh caches above
+    hand out fresh tensors when the host mesh changes."""
+    key = (cells_dev.data_ptr(), tuple(cells_dev.shape), tuple(cells_dev.stride()), cells_dev.device.index,
+           tile_cells)
     hit = _TILE_CACHE.get(key)
-    if hit is not None and hit[0] is cells_dev:
+    if hit is not None:  # (the cached tensor keeps that memory alive: same key, same storage; views match too)
         return hit[1]
     tiles = CellTiles(cells_dev, dim, tile_cells)
     while len(_TILE_CACHE) >= _TILE_CACHE_SIZE:
@@ -549,6 +557,85 @@ def integrate_mesh(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: Quadr
         if i >= 0:
             raise OrientationError(f"cell {i} is degenerate or negatively oriented")
     return res
+
+
+class ResidualGraph:
+    """``integrate_transposed`` for one fixed (mesh, layout, tabulation, rule,
+    form, aux, dtype) captured ONCE into a CUDA graph: every later residual
+    evaluation is a copy of the global vector into the graph's input buffer
+    and one graph replay (fused mesh kernel, f32 remainder cells, deterministic
+    scatter-add) -- no per-call Python dispatch, argument checks, cache
+    lookups or launch overhead (the device-resident call's ~0.1 ms host floor,
+    DESIGN.md §7).  For GPU-resident solver loops (Newton / Krylov iterations
+    over a static mesh).  Same bits as integrate_transposed.
+
+    The constructor runs one eager call (uploads and caches the mesh's device
+    data, builds the incidence and tile tables, compiles a run-time form, and
+    checks orientation -- OrientationError is raised there), then captures.
+    The mesh, aux and tabulation are frozen at construction (aux is copied);
+    build a new ResidualGraph after changing them.
+
+    ``graph(coeffs_global)`` -> the residual, a CUDA tensor owned by the graph
+    and overwritten by the next call (pass ``out=`` to copy it out).
+    ``coeffs_global``: CUDA tensor or numpy array of layout.global_size(mesh)
+    entries (held in float64, cast to the run dtype inside the graph)."""
+
+    def __init__(self, mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: QuadratureRule, form: PhysicsForm,
+                 aux: Optional[CellAux] = None, *, n_bl: int, n_cb: int, dtype="f64",
+                 cell_geom: Optional[CellGeometry] = None, **kwargs):
+        torch = _torch()
+        dt = scalar_dtype(dtype)
+        tdt = torch.float32 if dt == np.float32 else torch.float64
+        self.dtype = dt
+        self.n = layout.global_size(mesh)
+        # float64 input buffer (and aux copy) whatever the run precision: the f32 lane reads it cast once (in the graph),
+        # the f32 run's float64 remainder cells read it as given -- as integrate_transposed does with a
+        # float64 global vector (executor.py:258-264); an f32 input is copied in exactly
+        self.glob = torch.zeros(self.n, dtype=torch.float64, device="cuda")
+        del tdt
+        self.aux = None if aux is None else CellAux(aux.space, _dev(aux.values, torch, np.dtype(np.float64)).clone())
+        if cell_geom is not None:
+            cell_geom = CellGeometry(_dev(cell_geom.inv_jacobians, torch, dt).clone(),
+                                     _dev(cell_geom.determinants, torch, dt).clone())
+        call = dict(n_bl=n_bl, n_cb=n_cb, dtype=dt, cell_geom=cell_geom, **kwargs)
+        self._args = (mesh, layout, tab, rule, form)
+        kernel = _resolve_backend(kwargs.get("backend"), form, rule.n_q, aux, dt.itemsize)
+        if cell_geom is None and not isinstance(kernel, _backend.JitKernel) and not _mesh_fusable(tab, rule):
+            # the unfused path's geometry call synchronises (its orientation check): geometry once, here
+            cells_dev, verts_dev = _mesh_on_device(mesh, torch)
+            g = compute_geometry(mesh, cells=cells_dev, vertices=verts_dev, device_out=True)
+            call["cell_geom"] = CellGeometry(_dev(g.inv_jacobians, torch, dt), _dev(g.determinants, torch, dt))
+        self._call = call  # the graph reads these device tensors (given / precomputed geometry): keep them alive
+        # eager warm-up (caches, tables, compilation, the orientation check)
+        _, self.trace = integrate_transposed(*self._args, self.glob, self.aux, **call)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(self.graph, stream=side):
+                self.residual, _ = integrate_transposed(*self._args, self.glob, self.aux, check_orientation=False,
+                                                        **call)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        # the graph holds raw pointers into the cached device mesh data (connectivity, vertices, incidence,
+        # tile tables): keep those tensors alive past any later eviction from the module caches
+        self._keep = [list(c.values()) for c in (_MESH_CACHE, _INCIDENCE_CACHE, _TILE_CACHE, _PART_CACHE)]
+
+    def __call__(self, coeffs_global, out=None):
+        torch = _torch()
+        if isinstance(coeffs_global, np.ndarray) or not hasattr(coeffs_global, "is_cuda"):
+            src = torch.from_numpy(np.ascontiguousarray(coeffs_global, dtype=np.float64))
+        else:
+            src = coeffs_global
+        if int(src.numel()) != self.n:
+            raise ShapeError(f"global vector has {src.numel()} entries, expected {self.n}")
+        self.glob.copy_(src.reshape(-1), non_blocking=False)
+        self.graph.replay()
+        if out is not None:
+            out.copy_(self.residual)
+            return out
+        return self.residual
 
 
 def integrate_partitioned(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: QuadratureRule,

@@ -95,15 +95,15 @@ def test_tiled_bitwise_vs_oracle_and_per_cell_kernel(dim, n, shuffle, n_cells, f
 
 @pytest.mark.parametrize("tile", ["64", "96", "192", "256"])
 def test_tiled_tile_sizes(tile, monkeypatch):
-    """Every legal tile size (a multiple of n_b*n_q and of the warp slice, at
-    most 6 slices) gives the same bits; an illegal one is a ConfigurationError."""
+    """Every legal tile size (a multiple of n_b*n_q and of the warp slice,
+    at most 1024 vertex slots; > 6 slices loop over the consumer warps) gives the same bits; an illegal one is a ConfigurationError."""
     for dim in (2, 3):
         mesh, form, glob, aux = _problem(dim, 9 if dim == 3 else 40, txb.poisson_varcoef_form, "p0", seed=7)
         rule = txb.quadrature_rule(dim, 1)
         tab = txb.tabulate(dim, rule)
         ref = _oracle(mesh, form, glob, aux, rule, np.float64)
         monkeypatch.setenv("TXB_TILE_CELLS", tile)
-        ok = int(tile) % (dim + 1) == 0 and int(tile) % 32 == 0 and int(tile) // 32 <= 6
+        ok = int(tile) % (dim + 1) == 0 and int(tile) % 32 == 0 and int(tile) * (dim + 1) <= 1024
         g = torch.from_numpy(glob).cuda()
         if ok:
             out = txb.integrate_mesh(mesh, txb.FieldLayout(1), tab, rule, form, g, aux, dtype="f64")
@@ -159,7 +159,9 @@ def test_tiles_cached_per_connectivity_tensor():
     cells = torch.from_numpy(mesh.cells).cuda()
     a = executor.cell_tiles(cells, 3, 128)
     assert executor.cell_tiles(cells, 3, 128) is a
+    assert executor.cell_tiles(cells[:], 3, 128) is a  # a view of the same memory
     assert executor.cell_tiles(cells.clone(), 3, 128) is not a
+    assert executor.cell_tiles(cells[128:], 3, 128) is not a
     out1 = txb.integrate_mesh(mesh, txb.FieldLayout(1), tab, rule, form, torch.from_numpy(glob).cuda(), aux,
                               cells=cells)
     out2 = txb.integrate_mesh(mesh, txb.FieldLayout(1), tab, rule, form, torch.from_numpy(glob).cuda(), aux,

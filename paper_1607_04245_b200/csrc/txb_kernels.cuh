@@ -147,13 +147,15 @@ enum KernelFamily { FAMILY_CELLS = 0, FAMILY_MESH = 1, FAMILY_JIT = 2 };
 // measured on B200 (profiles/r1v_batch_sweep.md).  Launch-sized problems
 // (< 2^22 cells) favour smaller batches -- a shorter ramp and tail -- for the
 // cell-array kernels: 128 cells except the 2D configurations whose N_bc steps
-// are 96 cells, where 192 wins for scalar f32 and f64 elasticity; 96 KB in
+// are 96 cells, where 192 wins for scalar f32 and f64 elasticity (288 for f32
+// elasticity once scheduling is dynamic, profiles/r2w_sweep.md); 96 KB in
 // flight except 3D var-coef f64 (96 KB costs it an occupancy step: 26.0 ->
 // 31.4 us) and 2D var-coef f32.  Streaming-sized problems keep the batches that
 // amortise the per-batch overhead best (f32 256 cells: 3D var-coef f32 at 2^24
 // 190 vs 208 us), as do the mesh-fused and run-time compiled kernels.
 static int tuned_target_cells(const Config& c, int family, int64_t n_cells) {
   if (family != FAMILY_CELLS || n_cells >= ((int64_t)1 << 22)) return c.dtype == 8 ? 128 : 256;
+  if (c.dim == 2 && c.n_q == 1 && c.n_comp == 2 && c.dtype == 4) return 288;  // r2w: 12.27 -> 11.92 us
   if (c.dim == 2 && c.n_q == 1 && ((c.n_comp == 1 && c.dtype == 4) || (c.n_comp == 2 && c.dtype == 8))) return 192;
   return 128;
 }
@@ -386,11 +388,15 @@ static int compute_geometry(const Config& c, const KernelInfo& k, int64_t n_cell
   g.grid = (int)std::max<int64_t>(1, std::min<int64_t>(g.n_chunks, resident));
   // Default: dynamic batch scheduling so CTAs on SMs that get more bandwidth
   // take more batches and all finish together.  An explicit n_cb keeps the
-  // paper's static chunk order.  Only worth it when a batch is long enough to
-  // hide the scheduling request's latency (>= 10 KB per stage; measured with
-  // an atomic counter in round 1, profiles/r1_sweep.md).
+  // paper's static chunk order.  Round 1 (an atomic-counter scheduler) found
+  // it worth it only for >= 10 KB stages; with cluster launch control it wins
+  // for every launch of >= 2^18 cells whatever the stage size (2^20 cells:
+  // 2D var-coef f32 9.14 -> 8.45 us, 3D var-coef f32 13.49 -> 12.75, 2D
+  // var-coef f64 16.70 -> 15.73; profiles/r2v_dyn.md) and loses ~1 % on the
+  // 65,536-cell launch.
   const int dyn_env = env_int("TXB_DYNAMIC", -1);
-  g.dynamic = n_cb <= 0 && (dyn_env < 0 ? (stage >= 10 * 1024 || k.prefer_dynamic) : dyn_env != 0);
+  g.dynamic = n_cb <= 0 && (dyn_env < 0 ? (stage >= 10 * 1024 || k.prefer_dynamic || n_cells >= ((int64_t)1 << 18))
+                                         : dyn_env != 0);
   g.resident = 0;
   g.static_batches = 0;
   if (g.dynamic) {

@@ -5,7 +5,8 @@
 
 Covers the ahead-of-time integration kernel (all forms, f32/f64, n_q 1-3,
 static and dynamic batch scheduling, ragged tails, unaligned buffers), the
-fused mesh kernel (given and in-kernel geometry), gather, incidence build,
+fused mesh kernels (given geometry; in-kernel geometry per cell and over
+tiles with per-tile vertex tables), gather, incidence build,
 scatter-add, geometry, the run-time compiled kernel (cell arrays and mesh entry
 points) and the halo pack/assemble.
 Every result is checked against the oracle so a sanitizer run is also a
@@ -102,6 +103,34 @@ def main():
                 got.reshape(-1, form.n_comp)[ids] = vals.cpu().numpy().reshape(-1, form.n_comp)
             assert got.tobytes() == want.tobytes()
             checks += 4
+
+    # tiled mesh kernel (geometry + gather from per-tile vertex tables): shuffled numbering (uint16 local
+    # indices), partial last tile, both basis phases (midpoint in-lane, two-point transposed), P1 aux,
+    # an unaligned aux base (global-memory aux path), f32 and f64
+    rng = np.random.default_rng(12)
+    base = txb.generate_unit_simplex_mesh(3, 5)
+    perm = rng.permutation(base.n_vertices)
+    smesh = txb.Mesh(3, np.ascontiguousarray(base.vertices[np.argsort(perm)]),
+                     np.ascontiguousarray(perm[base.cells][rng.permutation(base.n_cells)][:700]))
+    for m in (smesh, txb.generate_unit_simplex_mesh(2, 13)):
+        dim = m.dim
+        form = txb.poisson_varcoef_form(dim)
+        glob = rng.standard_normal(m.n_vertices)
+        nodal = rng.uniform(0.5, 1.5, (m.n_vertices, 1))[m.cells]
+        inv, det = oracle.geometry(m.vertices, m.cells)
+        for rule in (txb.quadrature_rule(dim, 1), txb.two_point_rule(dim)):
+            tab = txb.tabulate(dim, rule)
+            for dt, tdt in ((np.float64, torch.float64), (np.float32, torch.float32)):
+                raw = torch.empty(nodal.size + 1, dtype=tdt, device="cuda")
+                av = raw[1:].view(nodal.shape)
+                av.copy_(dev(nodal, dt))
+                out = txb.integrate_mesh(m, txb.FieldLayout(1), tab, rule, form, dev(glob, dt), CellAux("p1", av),
+                                         dtype="f64" if dt == np.float64 else "f32")
+                torch.cuda.synchronize()
+                ref = oracle.integrate(1, 2, tab.basis, tab.basis_der, rule.weights, inv, det,
+                                       oracle.gather(m.cells, glob, 1), nodal, dt)
+                assert out.cpu().numpy().tobytes() == ref.tobytes(), (dim, rule.n_q, dt)
+                checks += 1
 
     # run-time compiled user forms
     for name in user_forms.SPECS:

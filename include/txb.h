@@ -180,9 +180,11 @@ int txb_integrate_mesh_tiled(int form_code, int aux_mode, int dtype_bytes, int d
 /* Test hook: the fused kernels' branch-free float64 geometry per cell
  * (reciprocal + one residual correction; ok[c] = 0 where a cell's scale is
  * outside the range where that is the correctly rounded quotient and the
- * kernels recompute it with division).  Device pointers, asynchronous. */
+ * kernels recompute it with division).  exact_zero = 1: zero numerators keep
+ * their sign (the run-time compiled kernels' variant).  Device pointers,
+ * asynchronous. */
 int txb_debug_geometry_fast(int dim, int64_t n_cells, const double* vertices, const int64_t* cells,
-                            double* inv_j, double* det_j, int32_t* ok, void* stream);
+                            double* inv_j, double* det_j, int32_t* ok, int exact_zero, void* stream);
 
 /* Gather per-cell coefficient blocks (device pointers):
  *   out[c][b][k] = global[cells[c][b] * n_comp + k],  cells int64 (n, n_b). */

@@ -238,7 +238,11 @@ __device__ __forceinline__ bool dd_range_bad(double x) {
   return (hi - 0x20B00000u > 0x3E800000u) & ((hi | lo) != 0u);
 }
 
-template <int D>
+// EXACT_ZERO: a zero numerator returns itself (+-0, = numpy's x / det for
+// det > 0) instead of +0 -- for callers that can see the sign of a zero
+// geometry entry (the run-time compiled user forms); then every accepted cell
+// is bit-identical to affine_inverse.
+template <int D, bool EXACT_ZERO = false>
 __device__ __forceinline__ bool affine_inverse_fast(const double (&X)[D + 1][D], double (&inv)[D * D], double& det) {
   double m[D][D];
 #pragma unroll
@@ -279,7 +283,8 @@ __device__ __forceinline__ bool affine_inverse_fast(const double (&X)[D + 1][D],
     const double x = num[i];
     bad |= dd_range_bad(x);
     const double q0 = __fma_rn(x, y, __dmul_rn(x, yl));
-    inv[i] = __fma_rn(__fma_rn(-q0, det, x), y, q0);
+    const double q = __fma_rn(__fma_rn(-q0, det, x), y, q0);
+    inv[i] = (EXACT_ZERO && x == 0.0) ? x : q;
   }
 #else
   const double y = __drcp_rn(det);
@@ -289,7 +294,8 @@ __device__ __forceinline__ bool affine_inverse_fast(const double (&X)[D + 1][D],
     bad |= dd_range_bad(x);
     const double q0 = __dmul_rn(x, y);
     const double q1 = __fma_rn(__fma_rn(-q0, det, x), y, q0);
-    inv[i] = __fma_rn(__fma_rn(-q1, det, x), y, q1);
+    const double q = __fma_rn(__fma_rn(-q1, det, x), y, q1);
+    inv[i] = (EXACT_ZERO && x == 0.0) ? x : q;
   }
 #endif
   return !bad;

@@ -175,7 +175,6 @@ struct TiledArgs {
   int out_vec;                 // out base 16-byte aligned: in-lane rows stored with vector stores
   uint32_t sleep_ns;           // producer / gatherer try_wait suspend hint (0: plain retry)
   uint32_t consumer_sleep_ns;  // consumer `ready` try_wait suspend hint (0: plain retry)
-  int debug;                   // DIAGNOSTIC (TXB_TILED_DEBUG): 1 skip geometry math, 2 skip the gathers
   Tabulation<T> tab;
 };
 
@@ -283,11 +282,7 @@ __device__ __forceinline__ void tiled_slice(const TiledArgs<T>& a, const unsigne
 #pragma unroll
       for (int i = 0; i < D; ++i) X[b][i] = sx[i * vpitch + ids[b]];
     double inv[DD], detd;
-    if (a.debug & 1) {  // DIAGNOSTIC: no geometry arithmetic (data dependencies kept)
-#pragma unroll
-      for (int i = 0; i < DD; ++i) inv[i] = X[i / D + 1][i % D] - X[0][i % D];
-      detd = X[1][0];
-    } else if (!affine_inverse_fast<D>(X, inv, detd)) affine_inverse<D>(X, inv, detd);  // rare: out-of-range scales
+    if (!affine_inverse_fast<D>(X, inv, detd)) affine_inverse<D>(X, inv, detd);  // rare: out-of-range scales
     if (q == 0 && a.bad && detd <= 0.0) atomicMin(a.bad, (unsigned long long)(c0_batch + cell));
     T J[DD];
 #pragma unroll
@@ -481,7 +476,7 @@ integrate_tiled_kernel(const __grid_constant__ TiledArgs<T> a) {
         const int cnt = rec[0];
         double* sx = reinterpret_cast<double*>(st + L::xyz_off(nbc, vrec));
         T* su = reinterpret_cast<T*>(st + L::u_off(nbc, vrec));
-        for (int j = lane; j < ((a.debug & 2) ? 0 : cnt); j += 32) {
+        for (int j = lane; j < cnt; j += 32) {
           const int64_t v = rec[4 + j];
 #pragma unroll
           for (int i = 0; i < D; ++i) cp_async<8>(sx + i * vpitch + j, a.vertices + v * D + i);
@@ -625,7 +620,6 @@ static int launch_tiled(const Config& c, const KernelInfo& k, Geometry g, int64_
   a.out_vec = al16(out);
   a.sleep_ns = (uint32_t)std::max(0, env_int("TXB_TILED_SLEEP_NS", 0));
   a.consumer_sleep_ns = (uint32_t)std::max(0, env_int("TXB_TILED_CONSUMER_SLEEP_NS", 20000));  // measured +2 %
-  a.debug = env_int("TXB_TILED_DEBUG", 0);
   fill_tab(a.tab, c.n_q, c.dim + 1, c.dim, basis, basis_der, weights);
   void* params[] = {&a};
   cudaLaunchConfig_t cfg = {};
@@ -648,7 +642,7 @@ static int launch_tiled(const Config& c, const KernelInfo& k, Geometry g, int64_
 template <int D>
 __global__ void geometry_fast_kernel(const double* __restrict__ vertices, const int64_t* __restrict__ cells,
                                      int64_t n, double* __restrict__ inv_out, double* __restrict__ det_out,
-                                     int32_t* __restrict__ ok_out) {
+                                     int32_t* __restrict__ ok_out, int exact_zero) {
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= n) return;
   double X[D + 1][D];
@@ -657,7 +651,7 @@ __global__ void geometry_fast_kernel(const double* __restrict__ vertices, const 
 #pragma unroll
     for (int i = 0; i < D; ++i) X[b][i] = vertices[cells[c * (D + 1) + b] * D + i];
   double inv[D * D], det;
-  ok_out[c] = affine_inverse_fast<D>(X, inv, det) ? 1 : 0;
+  ok_out[c] = (exact_zero ? affine_inverse_fast<D, true>(X, inv, det) : affine_inverse_fast<D>(X, inv, det)) ? 1 : 0;
 #pragma unroll
   for (int i = 0; i < D * D; ++i) inv_out[c * D * D + i] = inv[i];
   det_out[c] = det;
@@ -668,13 +662,13 @@ __global__ void geometry_fast_kernel(const double* __restrict__ vertices, const 
 using namespace txb;
 
 extern "C" int txb_debug_geometry_fast(int dim, int64_t n_cells, const double* vertices, const int64_t* cells,
-                                       double* inv_j, double* det_j, int32_t* ok, void* stream) {
+                                       double* inv_j, double* det_j, int32_t* ok, int exact_zero, void* stream) {
   if (n_cells <= 0) return TXB_OK;
   const unsigned blocks = (unsigned)((n_cells + 255) / 256);
   if (dim == 2)
-    geometry_fast_kernel<2><<<blocks, 256, 0, (cudaStream_t)stream>>>(vertices, cells, n_cells, inv_j, det_j, ok);
+    geometry_fast_kernel<2><<<blocks, 256, 0, (cudaStream_t)stream>>>(vertices, cells, n_cells, inv_j, det_j, ok, exact_zero);
   else if (dim == 3)
-    geometry_fast_kernel<3><<<blocks, 256, 0, (cudaStream_t)stream>>>(vertices, cells, n_cells, inv_j, det_j, ok);
+    geometry_fast_kernel<3><<<blocks, 256, 0, (cudaStream_t)stream>>>(vertices, cells, n_cells, inv_j, det_j, ok, exact_zero);
   else {
     set_error("dim must be 2 or 3");
     return TXB_E_UNSUPPORTED;

@@ -169,14 +169,17 @@ def test_tiles_cached_per_connectivity_tensor():
     assert bitwise_equal(out1.cpu().numpy(), out2.cpu().numpy())
 
 
+@pytest.mark.parametrize("exact_zero", [0, 1])
 @pytest.mark.parametrize("dim", [2, 3])
 @pytest.mark.parametrize("seed", [0, 1])
-def test_branch_free_geometry_is_correctly_rounded(dim, seed):
+def test_branch_free_geometry_is_correctly_rounded(dim, seed, exact_zero):
     """affine_inverse_fast (reciprocal pair + one Markstein correction, one
     range predicate per cell) against numpy's correctly rounded x / det on
     2^20 random simplices over 12 decades of scale: every cell it accepts is
     equal to numpy (zeros up to sign, which the fused kernels' +0-started
-    output chains cannot see); cells it rejects are redone exactly."""
+    output chains cannot see; with exact_zero -- the run-time compiled
+    kernels' variant -- bit for bit, signed zeros included); cells it rejects
+    are redone exactly."""
     import ctypes
 
     from paper_1607_04245_b200 import _lib
@@ -200,7 +203,7 @@ def test_branch_free_geometry_is_correctly_rounded(dim, seed):
     det_d = torch.empty(n, dtype=torch.float64, device="cuda")
     ok = torch.empty(n, dtype=torch.int32, device="cuda")
     _lib.check(_lib.lib().txb_debug_geometry_fast(dim, n, V.data_ptr(), C.data_ptr(), inv_d.data_ptr(),
-                                                  det_d.data_ptr(), ok.data_ptr(), None))
+                                                  det_d.data_ptr(), ok.data_ptr(), exact_zero, None))
     torch.cuda.synchronize()
     okh = ok.cpu().numpy().astype(bool)
     assert bitwise_equal(det_d.cpu().numpy(), det)
@@ -211,3 +214,5 @@ def test_branch_free_geometry_is_correctly_rounded(dim, seed):
     assert np.array_equal(a, b)  # == treats +0 and -0 as equal
     nz = b != 0
     assert np.array_equal(a[nz].view(np.int64), b[nz].view(np.int64))
+    if exact_zero:
+        assert np.array_equal(a.view(np.int64), b.view(np.int64))

@@ -479,9 +479,16 @@ def cell_tiles(cells_dev, dim: int, tile_cells: int) -> CellTiles:
     if hit is not None:  # (the cached tensor keeps that memory alive: same key, same storage; views match too)
         return hit[1]
     tiles = CellTiles(cells_dev, dim, tile_cells)
-    while len(_TILE_CACHE) >= _TILE_CACHE_SIZE:
+    size = lambda e: (e[0].numel() * e[0].element_size() + e[1].records.numel() * 4  # noqa: E731
+                      + e[1].local.numel())
+    budget = int(os.environ.get("TXB_TILE_CACHE_MB", "4096")) << 20
+    entry = (cells_dev, tiles)
+    # bounded: at most _TILE_CACHE_SIZE entries and TXB_TILE_CACHE_MB of tables + the connectivity
+    # they keep alive (oldest first out)
+    while _TILE_CACHE and (len(_TILE_CACHE) >= _TILE_CACHE_SIZE or
+                           sum(size(e) for e in _TILE_CACHE.values()) + size(entry) > budget):
         _TILE_CACHE.pop(next(iter(_TILE_CACHE)))
-    _TILE_CACHE[key] = (cells_dev, tiles)
+    _TILE_CACHE[key] = entry
     return tiles
 
 

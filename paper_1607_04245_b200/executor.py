@@ -626,8 +626,12 @@ class ResidualGraph:
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
         # the graph holds raw pointers into the cached device mesh data (connectivity, vertices, incidence,
-        # tile tables): keep those tensors alive past any later eviction from the module caches
-        self._keep = [list(c.values()) for c in (_MESH_CACHE, _INCIDENCE_CACHE, _TILE_CACHE, _PART_CACHE)]
+        # tile tables): keep THIS mesh's tensors alive past any later eviction from the module caches
+        cells_dev, verts_dev = _mesh_on_device(mesh, torch)
+        lo = cells_dev.data_ptr()
+        hi = lo + cells_dev.numel() * cells_dev.element_size()
+        self._keep = [cells_dev, verts_dev, _incidence_for(mesh, cells_dev),
+                      [t for k, t in _TILE_CACHE.items() if lo <= k[0] < hi]]
 
     def __call__(self, coeffs_global, out=None):
         torch = _torch()

@@ -154,8 +154,9 @@ int txb_integrate_mesh(int form_code, int aux_mode, int dtype_bytes, int dim, in
  *   local   (n_tiles * tile_cells, 4) uint8 (local_bytes 1: every count
  *           <= 256) or uint16 (2): each cell's vertex positions in its tile's
  *           list (2D: the 4th entry 0); both zero-initialised by the caller.
- * txb_tile_counts writes each tile's count (n_tiles int32) so the caller can
- * size vrec = 4 + max(count) rounded up to a multiple of 4; txb_tile_build
+ * txb_tile_counts writes each tile's count (n_tiles int32; -1 for a tile
+ * holding a vertex id outside [0, 2^31)) so the caller can size
+ * vrec = 4 + max(count) rounded up to a multiple of 4; txb_tile_build
  * fills records and local.  Connectivity int64 (n_cells, dim+1), vertex ids
  * < 2^31, tile_cells * (dim+1) <= 1024.  Asynchronous on `stream`. */
 int txb_tile_counts(int dim, int64_t n_cells, const int64_t* cells, int tile_cells, int32_t* counts,

@@ -82,8 +82,13 @@ __global__ void __launch_bounds__(1024) tile_build_kernel(const int64_t* __restr
   const int ncell = (int)min((int64_t)tile, n_cells - c0);
   const int nent = ncell * NB;
   constexpr unsigned long long NONE = ~0ull;
-  keys[i] = i < nent ? ((unsigned long long)cells[c0 * NB + i] << 11) | (unsigned long long)i : NONE;
-  __syncthreads();
+  const long long id = i < nent ? (long long)cells[c0 * NB + i] : 0;
+  keys[i] = i < nent ? ((unsigned long long)id << 11) | (unsigned long long)i : NONE;
+  // vertex ids must lie in [0, 2^31): report a tile holding any other id with count -1
+  if (__syncthreads_or(id < 0 || id >= (1LL << 31))) {
+    if (i == 0 && counts) counts[t] = -1;
+    return;
+  }
   for (int k = 2; k <= P; k <<= 1)
     for (int j = k >> 1; j > 0; j >>= 1) {
       const int x = i ^ j;

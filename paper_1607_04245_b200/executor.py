@@ -440,6 +440,8 @@ class CellTiles:
         s = _stream_ptr(torch)
         _lib.check(_lib.lib().txb_tile_counts(dim, n, cells_dev.data_ptr(), tile_cells, counts.data_ptr(), s),
                    "txb_tile_counts")
+        if self.n_tiles and int(counts.min().item()) < 0:
+            raise IndexError("cell connectivity holds vertex ids outside [0, 2^31) (tiled mesh kernel)")
         self.max_count = int(counts.max().item()) if self.n_tiles else 0
         self.vrec = 4 + max(4, -(-self.max_count // 4) * 4)
         self.local_bytes = 1 if self.max_count <= 256 else 2
@@ -585,7 +587,9 @@ class ResidualGraph:
     ``graph(coeffs_global)`` -> the residual, a CUDA tensor owned by the graph
     and overwritten by the next call (pass ``out=`` to copy it out).
     ``coeffs_global``: CUDA tensor or numpy array of layout.global_size(mesh)
-    entries (held in float64, cast to the run dtype inside the graph)."""
+    entries (held in float64, cast to the run dtype inside the graph).
+    One caller at a time: the input and residual buffers are the graph's own
+    (not thread-safe; replays are ordered on the caller's current stream)."""
 
     def __init__(self, mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: QuadratureRule, form: PhysicsForm,
                  aux: Optional[CellAux] = None, *, n_bl: int, n_cb: int, dtype="f64",

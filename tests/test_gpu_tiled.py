@@ -216,3 +216,12 @@ def test_branch_free_geometry_is_correctly_rounded(dim, seed, exact_zero):
     assert np.array_equal(a[nz].view(np.int64), b[nz].view(np.int64))
     if exact_zero:
         assert np.array_equal(a.view(np.int64), b.view(np.int64))
+
+
+def test_tile_builder_rejects_out_of_range_ids():
+    cells = torch.tensor([[0, 1, 2, 3], [1, 2, 3, (1 << 31) + 5]], dtype=torch.int64, device="cuda")
+    with pytest.raises(IndexError):
+        executor.CellTiles(cells, 3, 128)
+    cells = torch.tensor([[0, 1, 2, -1]], dtype=torch.int64, device="cuda")
+    with pytest.raises(IndexError):
+        executor.CellTiles(cells, 3, 128)

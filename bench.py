@@ -634,6 +634,24 @@ def time_e2e(wl, steps, warmup):
     return dt, h2d, out.nbytes, out
 
 
+def h2d_link_gbs(nbytes: int, reps: int = 5) -> float:
+    """Pinned host -> device copy rate of this box's link (cudaMemcpy of nbytes,
+    best of reps): the ceiling of the e2e path, whose inputs must cross it."""
+    import torch
+
+    src = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    dst = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    best = float("inf")
+    for _ in range(reps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+        best = min(best, time.perf_counter() - t0)
+    del src, dst
+    return nbytes / best / 1e9
+
+
 def stream_probe(read_b, write_b, reps=20):
     """Measured achievable HBM GB/s of a STREAM-like kernel at the kernel's read:write ratio."""
     import ctypes
@@ -963,6 +981,15 @@ def main():
                               f"{r['cores']} processes, median pass"}
             except Exception as e:  # noqa: BLE001
                 line["cpu_baseline"] = {"value": None, "error": f"{type(e).__name__}: {e}"}
+        if e2e_gf:
+            # what bounds e2e: the step's inputs cross the host link (context, not a second metric)
+            try:
+                link = h2d_link_gbs(h2d)
+                floor_ms = h2d / link / 1e6
+                line["e2e"].update({"h2d_link_gbs": link, "h2d_floor_ms_per_step": floor_ms,
+                                    "frac_of_h2d_floor": floor_ms / (e2e_s / e2e_steps * 1e3)})
+            except Exception as e:  # noqa: BLE001
+                line["e2e"]["h2d_link_error"] = f"{type(e).__name__}: {e}"
     try:
         # -------------------------------------------------------------- extras
         # (each row group guarded: a failure is an error row, never a lost headline)

@@ -513,7 +513,21 @@ def api_rows(steps=20):
     dt = (time.perf_counter() - t0) / steps
     rows.append({"config": "api_integrate_transposed_device_user_advect_3d_f64", "cells": mesh.n_cells,
                  "vertices": mesh.n_vertices, "ms_per_call": dt * 1e3, "gcells_per_s": mesh.n_cells / dt / 1e9,
-                 "path": "CUDA tensors in/out: run-time compiled form, mesh entry point + scatter-add"})
+                 "path": "CUDA tensors in/out: run-time compiled form, tiled mesh entry point + scatter-add"})
+    rg = txb.ResidualGraph(mesh, layout, tab, rule, form, aux_dev, n_bl=32, n_cb=8, dtype=dtype,
+                           shared_mem_limit=None)
+    for _ in range(3):
+        rg(glob_dev)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        rg(glob_dev)
+    e1.record()
+    torch.cuda.synchronize()
+    rows.append({"config": "api_residual_graph_device_user_advect_3d_f64", "cells": mesh.n_cells,
+                 "vertices": mesh.n_vertices, "device_ms_per_call": e0.elapsed_time(e1) / steps,
+                 "path": "ResidualGraph of the run-time compiled form (tiled mesh entry point + scatter-add)"})
     return rows
 
 

@@ -5,6 +5,7 @@
 
 #ifdef __CUDACC_RTC__
 typedef unsigned int uint32_t;
+typedef int int32_t;
 typedef unsigned long long uint64_t;
 typedef long long int64_t;
 typedef unsigned long long uintptr_t;
@@ -143,6 +144,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
+}
+
+// Element copy global -> shared (LDGSTS), BYTES = 4, 8 or 16.
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(dst)), "l"(src), "n"(BYTES) : "memory");
+}
+
+// The mbarrier receives one arrival when all of this thread's prior cp.async
+// copies have landed (noinc: the arrival is one of the barrier's expected count).
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 // Bulk prefetch of [src, src + bytes) into L2 (no completion, no data returned).

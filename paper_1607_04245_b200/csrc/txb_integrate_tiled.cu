@@ -201,17 +201,6 @@ struct TiledStage {
   __host__ __device__ static int stage_bytes(int n, int vrec) { return u_off(n, vrec) + u_bytes(vrec); }
 };
 
-template <int BYTES>
-__device__ __forceinline__ void cp_async(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(dst)), "l"(src), "n"(BYTES) : "memory");
-}
-
-// The mbarrier receives one arrival when all of this thread's prior cp.async
-// copies have landed (noinc: the arrival is one of the barrier's expected count).
-__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
 template <typename T, int N>
 __device__ __forceinline__ void store_row(T* __restrict__ p, const T (&r)[N], bool vec) {
   constexpr int BYTES = N * (int)sizeof(T);

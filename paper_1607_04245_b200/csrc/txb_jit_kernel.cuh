@@ -64,18 +64,27 @@ struct MeshIn {
   const real* glob;
   unsigned long long* bad;
   int64_t c0_batch;
+  // tiled entry points: the stage's local indices and its vertex table (structure of arrays)
+  const unsigned char* s_local;
+  const double* sx;
+  const real* su;
+  int vpitch, upitch, lb;
 };
+
+// Where a slice's per-cell inputs come from.
+enum { SRC_CELLS = 0, SRC_MESH = 1, SRC_TILED = 2 };
 
 __device__ __forceinline__ int inv_bytes(int n) { return round_up(n * DD * S, 16); }
 __device__ __forceinline__ int det_bytes(int n) { return round_up(n * S, 16); }
 __device__ __forceinline__ int coef_bytes(int n) { return round_up(n * NBC * S, 16); }
 __device__ __forceinline__ int aux_bytes(int n) { return round_up(n * AUXW * S, 16); }
 
-template <bool STD, bool VEC, bool MESH>
+template <bool STD, bool VEC, int SRC>
 __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const real* __restrict__ s_inv,
                                            const real* __restrict__ s_det, const real* __restrict__ s_coef,
                                            const real* __restrict__ s_aux, real* __restrict__ scratch, int c0,
                                            int ncell, real* __restrict__ out, int lane, const MeshIn& mi) {
+  constexpr bool MESH = SRC != SRC_CELLS;
   constexpr bool STAGE_T = STD && !MESH;
   real* s_tr = scratch;
   real* s_f1 = s_tr + P * Area<STAGE_T>::NTR;
@@ -93,17 +102,39 @@ __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const re
     if constexpr (MESH) {
       // gather (mesh.py:202-217) and float64 geometry (mesh.py:150-190), cast once to the run
       // precision (executor.py:77-90): the reference's host steps, in-kernel
-      int64_t ids[NB];
-      load_row<int64_t, NB, VEC>(mi.ids + cell * NB, ids);
-#pragma unroll
-      for (int b = 0; b < NB; ++b)
-#pragma unroll
-        for (int c = 0; c < NCOMP; ++c) cf[b * NCOMP + c] = __ldg(mi.glob + ids[b] * NCOMP + c);
       double X[NB][D];
+      if constexpr (SRC == SRC_TILED) {
+        // the tile's vertex table in shared memory, through the cell's local indices
+        int ids[NB];
+        if (mi.lb == 1) {
+          const uint32_t w = reinterpret_cast<const uint32_t*>(mi.s_local)[cell];
 #pragma unroll
-      for (int b = 0; b < NB; ++b)
+          for (int b = 0; b < NB; ++b) ids[b] = (w >> (8 * b)) & 0xffu;
+        } else {
+          const uint2 w = reinterpret_cast<const uint2*>(mi.s_local)[cell];
 #pragma unroll
-        for (int i = 0; i < D; ++i) X[b][i] = __ldg(mi.X + ids[b] * D + i);
+          for (int b = 0; b < NB; ++b) ids[b] = ((b < 2 ? w.x : w.y) >> (16 * (b & 1))) & 0xffffu;
+        }
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+          for (int c = 0; c < NCOMP; ++c) cf[b * NCOMP + c] = mi.su[c * mi.upitch + ids[b]];
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+          for (int i = 0; i < D; ++i) X[b][i] = mi.sx[i * mi.vpitch + ids[b]];
+      } else {
+        int64_t ids[NB];
+        load_row<int64_t, NB, VEC>(mi.ids + cell * NB, ids);
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+          for (int c = 0; c < NCOMP; ++c) cf[b * NCOMP + c] = __ldg(mi.glob + ids[b] * NCOMP + c);
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+          for (int i = 0; i < D; ++i) X[b][i] = __ldg(mi.X + ids[b] * D + i);
+      }
       double inv[DD], detd;
       // branch-free correctly rounded quotients, signed zeros kept (user forms may see them);
       // exact division for the rare out-of-range cell
@@ -256,6 +287,7 @@ __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const re
 
 template <bool STD, bool MESH>
 __device__ __forceinline__ void integrate_body(const IntegrateArgs<real>& a, const MeshLaunchArgs<real>* m) {
+  constexpr int SRC = MESH ? SRC_MESH : SRC_CELLS;
   constexpr int SCRATCH_BYTES = Area<STD && !MESH>::BYTES;
   extern __shared__ __align__(128) unsigned char smem[];
   const int nbc = a.n_bc;
@@ -317,7 +349,7 @@ __device__ __forceinline__ void integrate_body(const IntegrateArgs<real>& a, con
   real* scratch = reinterpret_cast<real*>(scratch_base + warp * SCRATCH_BYTES);
   pipeline_consume(a, p, smem, stage_bytes, [&](const unsigned char* st, int64_t c0, int ncell) {
     real* out = a.out + c0 * NBC;
-    MeshIn mi{nullptr, nullptr, nullptr, nullptr, c0};
+    MeshIn mi{nullptr, nullptr, nullptr, nullptr, c0, nullptr, nullptr, nullptr, 0, 0, 0};
     if constexpr (MESH) {
       mi.ids = st ? reinterpret_cast<const int64_t*>(st) : m->cells + c0 * NB;
       mi.X = m->vertices;
@@ -330,15 +362,131 @@ __device__ __forceinline__ void integrate_body(const IntegrateArgs<real>& a, con
       const real* s_coef = reinterpret_cast<const real*>(st + o_coef);
       const real* s_aux = reinterpret_cast<const real*>(st + o_aux);
       for (int c = warp * CW; c < ncell; c += W * CW)
-        warp_slice<STD, true, MESH>(a.tab, s_inv, s_det, s_coef, s_aux, scratch, c, ncell, out, lane, mi);
+        warp_slice<STD, true, SRC>(a.tab, s_inv, s_det, s_coef, s_aux, scratch, c, ncell, out, lane, mi);
     } else {
       // unaligned caller buffers or an odd-sized partial batch: straight from global memory
       const real* g_aux = AUXW ? a.aux + c0 * AUXW : nullptr;
       for (int c = warp * CW; c < ncell; c += W * CW)
-        warp_slice<STD, false, MESH>(a.tab, a.inv_j + c0 * DD, a.det_j + c0, a.coeffs + c0 * NBC, g_aux, scratch, c,
-                                     ncell, out, lane, mi);
+        warp_slice<STD, false, SRC>(a.tab, a.inv_j + c0 * DD, a.det_j + c0, a.coeffs + c0 * NBC, g_aux, scratch, c,
+                                    ncell, out, lane, mi);
     }
   });
+}
+
+// ---------------------------------------------------------------------------
+// Tiled mesh entry points (csrc/txb_integrate_tiled.cu's design): a batch is a
+// tile; the producer lane bulk-copies the tile's local indices, aux slice and
+// distinct-vertex record; the gatherer warp copies each distinct vertex's
+// coordinates and coefficients once into the stage's structure-of-arrays table
+// (cp.async, completion on `ready`); the consumers run the slices above with
+// their rows read from that table.
+// Stage: [local indices][aux][record][x | y (| z) float64][coefficient components]
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int t_local_bytes(int n, int lb) { return round_up(n * 4 * lb, 16); }
+__device__ __forceinline__ int t_xyz_pitch(int vrec) { return round_up(vrec * 8, 16) / 8; }
+__device__ __forceinline__ int t_u_pitch(int vrec) { return round_up(vrec * S, 16) / S; }
+
+template <bool STD>
+__device__ __forceinline__ void integrate_tiled_body(const TiledLaunchArgs<real>& t) {
+  const IntegrateArgs<real>& a = t.a;
+  constexpr int SCRATCH_BYTES = Area<false>::BYTES;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int nbc = a.n_bc, vrec = t.vrec, lb = t.lb;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int W = a.warps;
+  const int o_aux = t_local_bytes(nbc, lb);
+  const int o_rec = o_aux + aux_bytes(nbc);
+  const int o_xyz = o_rec + vrec * 4;
+  const int vpitch = t_xyz_pitch(vrec), upitch = t_u_pitch(vrec);
+  const int o_u = o_xyz + D * vpitch * 8;
+  const int stage_bytes = o_u + NCOMP * upitch * S;
+  unsigned char* scratch_base = smem + a.stages * stage_bytes;
+  const PipelineSmem p = carve_pipeline(scratch_base + W * SCRATCH_BYTES);
+  uint64_t* ready = reinterpret_cast<uint64_t*>(scratch_base + W * SCRATCH_BYTES + PIPELINE_SMEM_BYTES);
+  if (threadIdx.x == 0)
+    for (int s = 0; s < a.stages; ++s) mbar_init(&ready[s], 32);
+  pipeline_init(a, p);
+  if (warp == W && lane == 0) {
+    pipeline_first_batches(a, a.prefetch, [&](int64_t c0, int ncell) {
+      bulk_prefetch_l2(t.local + c0 * 4 * lb, (uint32_t)t_local_bytes(nbc, lb));
+      bulk_prefetch_l2(t.records + (c0 / nbc) * vrec, (uint32_t)(vrec * 4));
+    });
+  }
+  pipeline_wait_prior_grid();
+
+  if (warp == W) {
+    // ============================ producer lane ============================
+    if (lane != 0) return;
+    const uint64_t policy = l2_evict_first_policy();
+    pipeline_produce(a, p, smem, stage_bytes, [&](unsigned char* st, int64_t c0, int ncell, uint64_t* bar) {
+      const uint32_t lbytes = t_local_bytes(nbc, lb), rb = vrec * 4;
+      const uint32_t ab = ncell * AUXW * S;
+      const bool auxb = AUXW != 0 && t.aux_bulk && (ab & 15u) == 0;
+      mbar_arrive_expect_tx(bar, lbytes + rb + (auxb ? ab : 0));
+      bulk_g2s(st, t.local + c0 * 4 * lb, lbytes, bar, policy);
+      if (auxb) bulk_g2s(st + o_aux, a.aux + c0 * AUXW, ab, bar, policy);
+      bulk_g2s(st + o_rec, t.records + (c0 / nbc) * vrec, rb, bar, policy);
+      return true;
+    });
+    return;
+  }
+
+  if (warp == W + 1) {
+    // ============================ gatherer warp ============================
+    int stage = 0;
+    uint32_t phase = 0;
+    for (;;) {
+      mbar_wait(&p.full[stage], phase);
+      const int n = p.info_n[stage];
+      if (n != 0) {
+        unsigned char* st = smem + stage * stage_bytes;
+        const int32_t* rec = reinterpret_cast<const int32_t*>(st + o_rec);
+        const int cnt = rec[0];
+        double* sx = reinterpret_cast<double*>(st + o_xyz);
+        real* su = reinterpret_cast<real*>(st + o_u);
+        for (int j = lane; j < cnt; j += 32) {
+          const int64_t v = rec[4 + j];
+#pragma unroll
+          for (int i = 0; i < D; ++i) cp_async<8>(sx + i * vpitch + j, t.vertices + v * D + i);
+#pragma unroll
+          for (int c = 0; c < NCOMP; ++c) cp_async<S>(su + c * upitch + j, t.coeffs_global + v * NCOMP + c);
+        }
+      }
+      cp_async_arrive_noinc(&ready[stage]);
+      if (n == 0) break;
+      if (++stage == a.stages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    return;
+  }
+
+  // ============================ consumer warps ============================
+  real* scratch = reinterpret_cast<real*>(scratch_base + warp * SCRATCH_BYTES);
+  int stage = 0;
+  uint32_t phase = 0;
+  for (;;) {
+    mbar_wait(&ready[stage], phase);
+    mbar_wait(&p.full[stage], phase);
+    const int64_t c0 = p.info_c0[stage];
+    const int ncell = p.info_n[stage];
+    if (ncell == 0) break;
+    const unsigned char* st = smem + stage * stage_bytes;
+    const uint32_t ab = ncell * AUXW * S;
+    const real* aux_src = (AUXW != 0 && t.aux_bulk && (ab & 15u) == 0) ? reinterpret_cast<const real*>(st + o_aux)
+                                                                        : a.aux + c0 * AUXW;
+    MeshIn mi{nullptr, nullptr, nullptr, t.bad, c0, st, reinterpret_cast<const double*>(st + o_xyz),
+              reinterpret_cast<const real*>(st + o_u), vpitch, upitch, lb};
+    real* out = a.out + c0 * NBC;
+    for (int c = warp * CW; c < ncell; c += W * CW)
+      warp_slice<STD, true, SRC_TILED>(a.tab, nullptr, nullptr, nullptr, aux_src, scratch, c, ncell, out, lane, mi);
+    mbar_arrive(&p.empty[stage]);
+    if (++stage == a.stages) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
 }
 
 }  // namespace jit
@@ -367,5 +515,16 @@ txb_jit_integrate_mesh(const __grid_constant__ txb::MeshLaunchArgs<real> m) {
 extern "C" __global__ void __launch_bounds__(txb::MAX_CTA_THREADS, 1)
 txb_jit_integrate_mesh_std(const __grid_constant__ txb::MeshLaunchArgs<real> m) {
   txb::jit::integrate_body<true, true>(m.a, &m);
+}
+
+// tiled mesh entry points (geometry + gather from per-tile vertex tables)
+extern "C" __global__ void __launch_bounds__(txb::MAX_CTA_THREADS, 1)
+txb_jit_integrate_tiled(const __grid_constant__ txb::TiledLaunchArgs<real> t) {
+  txb::jit::integrate_tiled_body<false>(t);
+}
+
+extern "C" __global__ void __launch_bounds__(txb::MAX_CTA_THREADS, 1)
+txb_jit_integrate_tiled_std(const __grid_constant__ txb::TiledLaunchArgs<real> t) {
+  txb::jit::integrate_tiled_body<true>(t);
 }
 #endif

@@ -65,6 +65,23 @@ struct MeshLaunchArgs {
   unsigned long long* bad;      // lowered to the first cell with detJ <= 0 (NULL = no check)
 };
 
+// Arguments of a tiled mesh kernel (run-time compiled lane): the batch
+// pipeline's (a batch = one tile of tile_cells cells), the per-tile distinct
+// vertex records and local indices (txb_tile_build), vertex coordinates and the
+// global coefficient vector (gathered once per tile by the gatherer warp).
+template <typename T>
+struct TiledLaunchArgs {
+  IntegrateArgs<T> a;           // inv_j / det_j / coeffs unused
+  const double* vertices;       // (n_vertices, D)
+  const T* coeffs_global;       // (n_vertices * n_comp)
+  unsigned long long* bad;      // lowered to the first cell with detJ <= 0 (NULL = no check)
+  const int32_t* records;       // (n_tiles, vrec): [count, 0, 0, 0, ids...]
+  const unsigned char* local;   // (n_tiles * tile, 4) uint8 | uint16
+  int vrec;
+  int lb;                       // local index bytes, 1 | 2
+  int aux_bulk;                 // aux base 16-byte aligned
+};
+
 // 16- and 8-byte vector types per element type (type-preserving: the lanes of
 // the vector ARE elements of the row, no conversion).
 template <typename T> struct Vec16;

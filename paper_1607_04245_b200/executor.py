@@ -390,12 +390,22 @@ def _jit_mesh(kernel, mesh: Mesh, tab: Tabulation, rule: QuadratureRule, form: P
     bad = torch.full((1,), -1, dtype=torch.int64, device="cuda") if check_orientation else None
     B, D, W = (np.ascontiguousarray(x, dtype=dt) for x in (tab.basis, tab.basis_der, rule.weights))
     av = None if aux_dev is None else aux_dev.values.contiguous()
-    rc = _lib.lib().txb_jit_integrate_mesh(ctypes.c_void_p(kernel.handle), n, mesh.n_vertices, B.ctypes.data,
-                                           D.ctypes.data, W.ctypes.data, verts_dev.data_ptr(), cells_dev.data_ptr(),
-                                           glob_dev.data_ptr(), None if av is None else av.data_ptr(),
-                                           res.data_ptr(), None if bad is None else bad.data_ptr(), n_bl,
-                                           _stream_ptr(torch))
-    _lib.check(rc, "txb_jit_integrate_mesh")
+    if n > 0 and _tiled_enabled(mesh, rule):
+        # per-tile vertex tables (the tiled kernel's design, run-time compiled form)
+        tiles = cell_tiles(cells_dev, mesh.dim, default_tile_cells(mesh.dim, rule.n_q))
+        rc = _lib.lib().txb_jit_integrate_mesh_tiled(
+            ctypes.c_void_p(kernel.handle), n, mesh.n_vertices, B.ctypes.data, D.ctypes.data, W.ctypes.data,
+            verts_dev.data_ptr(), tiles.tile_cells, tiles.records.data_ptr(), tiles.vrec, tiles.local.data_ptr(),
+            tiles.local_bytes, glob_dev.data_ptr(), None if av is None else av.data_ptr(), res.data_ptr(),
+            None if bad is None else bad.data_ptr(), _stream_ptr(torch))
+        _lib.check(rc, "txb_jit_integrate_mesh_tiled")
+    else:
+        rc = _lib.lib().txb_jit_integrate_mesh(ctypes.c_void_p(kernel.handle), n, mesh.n_vertices, B.ctypes.data,
+                                               D.ctypes.data, W.ctypes.data, verts_dev.data_ptr(),
+                                               cells_dev.data_ptr(), glob_dev.data_ptr(),
+                                               None if av is None else av.data_ptr(), res.data_ptr(),
+                                               None if bad is None else bad.data_ptr(), n_bl, _stream_ptr(torch))
+        _lib.check(rc, "txb_jit_integrate_mesh")
     if bad is not None:
         i = int(bad.item())
         if i >= 0:

@@ -257,13 +257,16 @@ def test_jit_standard_table_entry_point_matches_generic(name, dim, monkeypatch):
 @pytest.mark.parametrize("name", SPECS)
 @pytest.mark.parametrize("dim", [2, 3])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
-def test_integrate_transposed_user_forms_mesh_fused(name, dim, dtype):
+@pytest.mark.parametrize("tiled", ["1", "0"])
+def test_integrate_transposed_user_forms_mesh_fused(name, dim, dtype, tiled, monkeypatch):
     """integrate_transposed with a run-time compiled form: the mesh entry point
     (float64 geometry + gather in-kernel, txb_jit_integrate_mesh) on a perturbed
     Kuhn mesh with a shuffled vertex numbering, midpoint and two-point rules,
     then the scatter-add — bit-identical to the oracle's geometry -> gather ->
     python-lane integration -> np.add.at, and to the unfused route (given
-    geometry: gather + txb_jit_integrate)."""
+    geometry: gather + txb_jit_integrate).  tiled = 1: the tiled mesh entry
+    point (txb_jit_integrate_mesh_tiled, per-tile vertex tables)."""
+    monkeypatch.setenv("TXB_TILED", tiled)
     s = user_forms.spec(name, dim)
     f = form_of(name, dim)
     npdt = np.float64 if dtype == "f64" else np.float32

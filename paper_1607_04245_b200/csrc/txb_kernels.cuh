@@ -294,10 +294,8 @@ static int compute_geometry(const Config& c, const KernelInfo& k, int64_t n_cell
   const int wcap = std::max(1, std::min(k.max_warps > 0 ? k.max_warps : MAX_CONSUMER_WARPS,
                                         env_int("TXB_MAX_WARPS", MAX_CONSUMER_WARPS)));
   g.warps = std::min(wcap, slices);
-  g.threads = 32 * (g.warps + 1 + k.extra_warps);
 
   const int stage = k.stage(g.n_bc);
-  const int fixed = g.warps * k.scratch_bytes(g.n_bc) + PIPELINE_SMEM_BYTES + 16 + k.fixed_extra;
   int smem_cap = 227 * 1024;
   int dev = 0, sms = 148;
   if (query_device && cudaGetDevice(&dev) == cudaSuccess) {
@@ -305,6 +303,14 @@ static int compute_geometry(const Config& c, const KernelInfo& k, int64_t n_cell
     if (p.smem_optin > 0) smem_cap = p.smem_optin;
     if (p.sms > 0) sms = p.sms;
   }
+  // Large warp-private exchange areas (many quadrature points, big batches) may
+  // not fit next to a 2-stage ring with one consumer warp per slice: fewer
+  // consumer warps then loop over the batch's slices.
+  const int scratch_w = k.scratch_bytes(g.n_bc);
+  auto fixed_for = [&](int w) { return w * scratch_w + PIPELINE_SMEM_BYTES + 16 + k.fixed_extra; };
+  while (g.warps > 1 && fixed_for(g.warps) + 2 * stage > smem_cap) --g.warps;
+  g.threads = 32 * (g.warps + 1 + k.extra_warps);
+  const int fixed = fixed_for(g.warps);
   // Ring depth: keep about TXB_INFLIGHT_KB (72 KB) of batch loads in flight
   // per SM -- (CTAs/SM) x (stages-1) x stage bytes ~ HBM bandwidth x latency
   // per SM.  Deeper rings only queue more requests and lengthen the launch

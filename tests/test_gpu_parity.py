@@ -372,3 +372,23 @@ def test_random_problems_bitwise(dim, form, n_q, n, dtype, tables, n_bl, n_cb, o
     out = _run_device(fc, am, B, D, W, inv, det, co, aux, dtype, n_bl=n_bl, n_cb=n_cb, offset=offset)
     ref = oracle.integrate(fc, am, B, D, W, inv, det, co, aux, DT[dtype][0])
     assert bitwise_equal(out, ref)
+
+
+@pytest.mark.parametrize("dim,fc,am,n_q,n_bl", [(3, 1, 2, 8, 17), (3, 0, 0, 8, 17), (2, 1, 1, 8, 30),
+                                                  (3, 2, 0, 4, 8)])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_large_exchange_area_fits_by_fewer_warps(dim, fc, am, n_q, n_bl, dtype):
+    """Many quadrature points x big batches: one consumer warp per slice would
+    not fit the shared memory next to a 2-stage ring (found by the property
+    test: 3D, n_q 8, n_bl 17, f64 needs ~245 KB); fewer consumer warps loop
+    over the slices instead of raising CapacityError -- same bits."""
+    rng = np.random.default_rng(n_q * 100 + n_bl)
+    nb, nc = dim + 1, dim if fc == 2 else 1
+    n = 4000
+    B, D, W = rng.uniform(0, 1, (n_q, nb)), rng.uniform(-1, 1, (n_q, nb, dim)), rng.uniform(0.1, 0.5, n_q)
+    jac = np.eye(dim) + 0.3 * rng.uniform(-1, 1, (n, dim, dim))
+    inv, det = np.linalg.inv(jac), np.linalg.det(jac)
+    co = rng.standard_normal((n, nb, nc))
+    aux = None if am == 0 else (rng.uniform(0.5, 1.5, (n, 1)) if am == 1 else rng.uniform(0.5, 1.5, (n, nb, 1)))
+    out = _run_device(fc, am, B, D, W, inv, det, co, aux, dtype, n_bl=n_bl, n_cb=0, offset=0)
+    assert bitwise_equal(out, oracle.integrate(fc, am, B, D, W, inv, det, co, aux, DT[dtype][0]))

@@ -315,9 +315,9 @@ def time_mesh(name, steps, warmup, n_sets_min=4, given_geometry=False, tiled=Tru
     s = np.dtype(npdt).itemsize
     per_cell = (dim + 1) * 8 + (s if aux_space == "p0" else 0) + (dim + 1) * form.n_comp * s
     cells0 = torch.from_numpy(mesh.cells).cuda()
-    os.environ["TXB_TILED"] = "1" if tiled and not given_geometry else "0"
+    os.environ["TXB_TILED"] = "1" if tiled else "0"
     tiles = None
-    if tiled and not given_geometry:
+    if tiled:
         from paper_1607_04245_b200 import executor
 
         tiles = executor.cell_tiles(cells0, dim, executor.default_tile_cells(dim, 1))
@@ -829,18 +829,21 @@ def mesh_rows(peak, steps):
     rows = []
     for v in ("3d_varcoef_f64", "3d_varcoef_f32", "3d_elasticity_f64", "3d_elasticity_f32", "2d_varcoef_f64",
               "2d_varcoef_f32"):
-        for mode in ("given", "tiled", "per_cell"):
+        for mode in ("given", "given_tiled", "tiled", "per_cell"):
             def one(v=v, mode=mode):
                 vf, _ = config_model(v)
                 n = CONFIGS[v][3]
-                ms, per_cell = time_mesh(v, variant_steps(n, steps), 5, given_geometry=mode == "given",
-                                         tiled=mode == "tiled")
-                path = {"given": "txb_integrate_mesh: gather fused into the integration, geometry streamed",
+                ms, per_cell = time_mesh(v, variant_steps(n, steps), 5, given_geometry=mode.startswith("given"),
+                                         tiled=mode in ("tiled", "given_tiled"))
+                path = {"given": "txb_integrate_mesh: gather per cell fused into the integration, geometry streamed",
+                        "given_tiled": "txb_integrate_mesh_tiled: geometry streamed, coefficients from per-tile "
+                                       "vertex tables",
                         "per_cell": "txb_integrate_mesh: float64 geometry + gather per cell in-kernel",
                         "tiled": "txb_integrate_mesh_tiled: float64 geometry + gather from per-tile vertex "
                                  "tables in shared memory"}[mode]
                 return [{
-                    "config": {"given": "mesh_given_geometry_", "tiled": "mesh_tiled_geometry_in_kernel_",
+                    "config": {"given": "mesh_given_geometry_", "given_tiled": "mesh_tiled_given_geometry_",
+                               "tiled": "mesh_tiled_geometry_in_kernel_",
                                "per_cell": "mesh_geometry_in_kernel_"}[mode] + v,
                     "path": path,
                     "cells": n, "launch_ms": ms, "gflops": vf * n / (ms * 1e-3) / 1e9,

@@ -164,19 +164,20 @@ int txb_tile_counts(int dim, int64_t n_cells, const int64_t* cells, int tile_cel
 int txb_tile_build(int dim, int64_t n_cells, const int64_t* cells, int tile_cells, int vrec, int local_bytes,
                    int32_t* records, void* local, void* stream);
 
-/* txb_integrate_mesh with the geometry computed in-kernel, over the tiles
- * above (records / local 16-byte aligned): per tile, each distinct vertex's
- * coordinates and coefficients are gathered ONCE into shared memory and the
- * cells read them through their local indices.  tile_cells must be a
+/* txb_integrate_mesh over the tiles above (records / local 16-byte aligned):
+ * per tile, each distinct vertex's coefficients (and, with inv_j = det_j =
+ * NULL, coordinates: geometry computed in-kernel) are gathered ONCE into
+ * shared memory and the cells read them through their local indices; given
+ * geometry (inv_j / det_j in the run precision) streams with the batch.  tile_cells must be a
  * multiple of (dim+1)*n_q and of 32/n_q with at most 6 warp slices (3D: 128,
  * 2D: 96 or 192 for the midpoint rule).  Same results, bit for bit, as
- * txb_integrate_mesh with inv_j = det_j = NULL; bad_cell as there. */
+ * txb_integrate_mesh with the same inv_j / det_j; bad_cell as there. */
 int txb_integrate_mesh_tiled(int form_code, int aux_mode, int dtype_bytes, int dim, int n_q, int n_comp,
                              int64_t n_cells, int64_t n_vertices,
                              const void* basis, const void* basis_der, const void* weights,
                              const double* vertices, int tile_cells, const int32_t* records, int vrec,
-                             const void* local, int local_bytes, const void* coeffs_global, const void* aux,
-                             void* out, int64_t* bad_cell, void* stream);
+                             const void* local, int local_bytes, const void* coeffs_global, const void* inv_j,
+                             const void* det_j, const void* aux, void* out, int64_t* bad_cell, void* stream);
 
 /* Test hook: the fused kernels' branch-free float64 geometry per cell
  * (reciprocal + one residual correction; ok[c] = 0 where a cell's scale is

@@ -173,29 +173,36 @@ struct TiledArgs {
   const unsigned char* local;  // (n_tiles * tile, 4) uint8 | uint16
   const T* coeffs_global;      // (n_vertices * NCOMP)
   const T* aux;                // (n, 1) P0 | (n, D+1, 1) P1 | NULL
+  const T* inv_j;              // GEOM == 1: the caller's geometry (n, D, D) and (n), run precision
+  const T* det_j;
   T* out;                      // (n, D+1, NCOMP)
   unsigned long long* bad;     // lowered to the first cell with detJ <= 0 (NULL = no check)
   int vrec;                    // int32 per tile record (multiple of 4): 4 + the largest count, rounded
   int aux_bulk;                // aux base 16-byte aligned: full batches' aux slices arrive by bulk copy
+  int geom_bulk;               // GEOM == 1: inv_j / det_j bases 16-byte aligned (bulk copies, else global loads)
   int out_vec;                 // out base 16-byte aligned: in-lane rows stored with vector stores
   uint32_t sleep_ns;           // producer / gatherer try_wait suspend hint (0: plain retry)
   uint32_t consumer_sleep_ns;  // consumer `ready` try_wait suspend hint (0: plain retry)
   Tabulation<T> tab;
 };
 
-// Stage: [local indices][aux][record][x | y (| z) float64][coefficient components]
-template <typename T, int D, int NCOMP, int AUX, int LB>
+// Stage: [local indices][aux][GEOM: inv_j | det_j][record][coordinates (GEOM 0)][coefficient components]
+template <typename T, int D, int NCOMP, int AUX, int LB, int GEOM>
 struct TiledStage {
   static constexpr int NB = D + 1;
   static constexpr int AUXW = AUX == 1 ? 1 : (AUX == 2 ? NB : 0);
   __host__ __device__ static int local_bytes(int n) { return round_up(n * 4 * LB, 16); }
   __host__ __device__ static int aux_bytes(int n) { return round_up(n * AUXW * (int)sizeof(T), 16); }
+  __host__ __device__ static int inv_bytes(int n) { return GEOM ? round_up(n * D * D * (int)sizeof(T), 16) : 0; }
+  __host__ __device__ static int det_bytes(int n) { return GEOM ? round_up(n * (int)sizeof(T), 16) : 0; }
   __host__ __device__ static int rec_bytes(int vrec) { return vrec * 4; }
-  __host__ __device__ static int xyz_bytes(int vrec) { return D * round_up(vrec * 8, 16); }
+  __host__ __device__ static int xyz_bytes(int vrec) { return GEOM ? 0 : D * round_up(vrec * 8, 16); }
   __host__ __device__ static int u_pitch(int vrec) { return round_up(vrec * (int)sizeof(T), 16) / (int)sizeof(T); }
   __host__ __device__ static int u_bytes(int vrec) { return NCOMP * u_pitch(vrec) * (int)sizeof(T); }
   __host__ __device__ static int aux_off(int n) { return local_bytes(n); }
-  __host__ __device__ static int rec_off(int n) { return local_bytes(n) + aux_bytes(n); }
+  __host__ __device__ static int inv_off(int n) { return local_bytes(n) + aux_bytes(n); }
+  __host__ __device__ static int det_off(int n) { return inv_off(n) + inv_bytes(n); }
+  __host__ __device__ static int rec_off(int n) { return det_off(n) + det_bytes(n); }
   __host__ __device__ static int xyz_off(int n, int vrec) { return rec_off(n) + rec_bytes(vrec); }
   __host__ __device__ static int u_off(int n, int vrec) { return xyz_off(n, vrec) + xyz_bytes(vrec); }
   __host__ __device__ static int stage_bytes(int n, int vrec) { return u_off(n, vrec) + u_bytes(vrec); }
@@ -236,10 +243,11 @@ __device__ __forceinline__ void store_row(T* __restrict__ p, const T (&r)[N], bo
 }
 
 // One warp slice of CW cells: c0 = batch-local first cell.
-template <typename T, int D, int NQ, int NCOMP, int FORM, int AUX, int LB, bool XP>
+template <typename T, int D, int NQ, int NCOMP, int FORM, int AUX, int LB, bool XP, int GEOM>
 __device__ __forceinline__ void tiled_slice(const TiledArgs<T>& a, const unsigned char* __restrict__ s_local,
                                             const T* __restrict__ aux_src, const double* __restrict__ sx,
-                                            const T* __restrict__ su, int vpitch, int upitch,
+                                            const T* __restrict__ su, const T* __restrict__ g_inv,
+                                            const T* __restrict__ g_det, int vpitch, int upitch,
                                             unsigned char* __restrict__ scratch, int64_t c0_batch, int c0,
                                             int ncell, int lane) {
   constexpr int NB = D + 1, DD = D * D, NBC = NB * NCOMP;
@@ -270,18 +278,28 @@ __device__ __forceinline__ void tiled_slice(const TiledArgs<T>& a, const unsigne
     for (int b = 0; b < NB; ++b)
 #pragma unroll
       for (int c = 0; c < NCOMP; ++c) cf[b * NCOMP + c] = su[c * upitch + ids[b]];
-    double X[NB][D];
-#pragma unroll
-    for (int b = 0; b < NB; ++b)
-#pragma unroll
-      for (int i = 0; i < D; ++i) X[b][i] = sx[i * vpitch + ids[b]];
-    double inv[DD], detd;
-    if (!affine_inverse_fast<D>(X, inv, detd)) affine_inverse<D>(X, inv, detd);  // rare: out-of-range scales
-    if (q == 0 && a.bad && detd <= 0.0) atomicMin(a.bad, (unsigned long long)(c0_batch + cell));
     T J[DD];
+    T det;
+    if constexpr (GEOM) {
+      // the caller's geometry in the run precision (stage or global)
 #pragma unroll
-    for (int i = 0; i < DD; ++i) J[i] = (T)inv[i];  // executor._device_arrays: cast once
-    const T det = (T)detd;
+      for (int i = 0; i < DD; ++i) J[i] = g_inv[cell * DD + i];
+      det = g_det[cell];
+      (void)sx;
+      (void)vpitch;
+    } else {
+      double X[NB][D];
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int i = 0; i < D; ++i) X[b][i] = sx[i * vpitch + ids[b]];
+      double inv[DD], detd;
+      if (!affine_inverse_fast<D>(X, inv, detd)) affine_inverse<D>(X, inv, detd);  // rare: out-of-range scales
+      if (q == 0 && a.bad && detd <= 0.0) atomicMin(a.bad, (unsigned long long)(c0_batch + cell));
+#pragma unroll
+      for (int i = 0; i < DD; ++i) J[i] = (T)inv[i];  // executor._device_arrays: cast once
+      det = (T)detd;
+    }
 
     // standard P1 pull-back (exactness note in txb_kernels.cuh)
     T tr[NB][D];
@@ -406,10 +424,10 @@ constexpr int TILED_MAX_THREADS = 32 * (TILED_MAX_CONSUMER_WARPS + 2);
 #define TXB_TILED_MIN_BLOCKS(NCOMP) ((NCOMP) == 1 ? 3 : 2)
 #endif
 
-template <typename T, int D, int NQ, int NCOMP, int FORM, int AUX, int LB, bool XP>
+template <typename T, int D, int NQ, int NCOMP, int FORM, int AUX, int LB, bool XP, int GEOM>
 __global__ void __launch_bounds__(TILED_MAX_THREADS, TXB_TILED_MIN_BLOCKS(NCOMP))
 integrate_tiled_kernel(const __grid_constant__ TiledArgs<T> a) {
-  using L = TiledStage<T, D, NCOMP, AUX, LB>;
+  using L = TiledStage<T, D, NCOMP, AUX, LB, GEOM>;
   using S = MeshScratch<T, D, NQ, NCOMP>;
   constexpr int NB = D + 1;
   constexpr int SCR = XP ? S::BYTES : 0;
@@ -445,9 +463,15 @@ integrate_tiled_kernel(const __grid_constant__ TiledArgs<T> a) {
       const uint32_t lbytes = L::local_bytes(nbc), rb = L::rec_bytes(vrec);
       const uint32_t ab = ncell * L::AUXW * (uint32_t)sizeof(T);
       const bool auxb = AUX != 0 && a.aux_bulk && (ab & 15u) == 0;
-      mbar_arrive_expect_tx(bar, lbytes + rb + (auxb ? ab : 0));
+      const uint32_t ib = GEOM ? ncell * D * D * (uint32_t)sizeof(T) : 0, db = GEOM ? ncell * (uint32_t)sizeof(T) : 0;
+      const bool geob = GEOM && a.geom_bulk && ((ib | db) & 15u) == 0;
+      mbar_arrive_expect_tx(bar, lbytes + rb + (auxb ? ab : 0) + (geob ? ib + db : 0));
       bulk_g2s(st, a.local + c0 * 4 * LB, lbytes, bar, policy);
       if (auxb) bulk_g2s(st + L::aux_off(nbc), a.aux + c0 * L::AUXW, ab, bar, policy);
+      if (geob) {
+        bulk_g2s(st + L::inv_off(nbc), a.inv_j + c0 * D * D, ib, bar, policy);
+        bulk_g2s(st + L::det_off(nbc), a.det_j + c0, db, bar, policy);
+      }
       bulk_g2s(st + L::rec_off(nbc), a.records + (c0 / nbc) * vrec, rb, bar, policy);
       return true;
     }, a.sleep_ns);
@@ -472,8 +496,10 @@ integrate_tiled_kernel(const __grid_constant__ TiledArgs<T> a) {
         T* su = reinterpret_cast<T*>(st + L::u_off(nbc, vrec));
         for (int j = lane; j < cnt; j += 32) {
           const int64_t v = rec[4 + j];
+          if constexpr (!GEOM) {
 #pragma unroll
-          for (int i = 0; i < D; ++i) cp_async<8>(sx + i * vpitch + j, a.vertices + v * D + i);
+            for (int i = 0; i < D; ++i) cp_async<8>(sx + i * vpitch + j, a.vertices + v * D + i);
+          }
 #pragma unroll
           for (int c = 0; c < NCOMP; ++c)
             cp_async<(int)sizeof(T)>(su + c * upitch + j, a.coeffs_global + v * NCOMP + c);
@@ -511,9 +537,17 @@ integrate_tiled_kernel(const __grid_constant__ TiledArgs<T> a) {
     }
     const double* sx = reinterpret_cast<const double*>(st + L::xyz_off(nbc, vrec));
     const T* su = reinterpret_cast<const T*>(st + L::u_off(nbc, vrec));
+    const T* g_inv = nullptr;
+    const T* g_det = nullptr;
+    if constexpr (GEOM) {
+      const uint32_t ib = ncell * D * D * (uint32_t)sizeof(T), db = ncell * (uint32_t)sizeof(T);
+      const bool geob = a.geom_bulk && ((ib | db) & 15u) == 0;
+      g_inv = geob ? reinterpret_cast<const T*>(st + L::inv_off(nbc)) : a.inv_j + c0 * D * D;
+      g_det = geob ? reinterpret_cast<const T*>(st + L::det_off(nbc)) : a.det_j + c0;
+    }
     for (int c = warp * CW; c < ncell; c += W * CW)
-      tiled_slice<T, D, NQ, NCOMP, FORM, AUX, LB, XP>(a, st, aux_src, sx, su, vpitch, upitch, scratch, c0, c,
-                                                      ncell, lane);
+      tiled_slice<T, D, NQ, NCOMP, FORM, AUX, LB, XP, GEOM>(a, st, aux_src, sx, su, g_inv, g_det, vpitch, upitch,
+                                                            scratch, c0, c, ncell, lane);
     mbar_arrive(&p.empty[stage]);
     if (++stage == a.stages) {
       stage = 0;
@@ -526,22 +560,24 @@ integrate_tiled_kernel(const __grid_constant__ TiledArgs<T> a) {
 // ---------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------
-template <typename T, int D, int NQ, int NCOMP, int FORM, int AUX, int LB, bool XP>
+template <typename T, int D, int NQ, int NCOMP, int FORM, int AUX, int LB, bool XP, int GEOM>
 struct TiledKernel {
-  using L = TiledStage<T, D, NCOMP, AUX, LB>;
-  static void* fn() { return (void*)integrate_tiled_kernel<T, D, NQ, NCOMP, FORM, AUX, LB, XP>; }
-  static int stage_bytes(int n_bc) { return L::local_bytes(n_bc) + L::aux_bytes(n_bc); }
+  using L = TiledStage<T, D, NCOMP, AUX, LB, GEOM>;
+  static void* fn() { return (void*)integrate_tiled_kernel<T, D, NQ, NCOMP, FORM, AUX, LB, XP, GEOM>; }
+  static int stage_bytes(int n_bc) {
+    return L::local_bytes(n_bc) + L::aux_bytes(n_bc) + L::inv_bytes(n_bc) + L::det_bytes(n_bc);
+  }
   static int scratch(int) { return XP ? MeshScratch<T, D, NQ, NCOMP>::BYTES : 0; }
   static int vrec_bytes(int vrec) { return L::rec_bytes(vrec) + L::xyz_bytes(vrec) + L::u_bytes(vrec); }
 };
 
 // In-lane basis phase for the midpoint rule (TXB_TILED_XPOSE=1 forces the
 // exchange-area transposition there too, for measurement).
-template <typename T, int D, int NQ, int LB>
+template <typename T, int D, int NQ, int LB, int GEOM>
 static bool pick_tiled_form(const Config& c, int vrec, bool xpose, KernelInfo& k) {
 #define TXB_TK(NCOMP, FORM, AUX, XP)                                        \
   {                                                                         \
-    using K = TiledKernel<T, D, NQ, NCOMP, FORM, AUX, LB, XP>;              \
+    using K = TiledKernel<T, D, NQ, NCOMP, FORM, AUX, LB, XP, GEOM>;        \
     k = {K::fn(), K::stage_bytes, K::scratch, 32 / NQ};                     \
     k.family = FAMILY_MESH;                                                 \
     k.stage_extra = K::vrec_bytes(vrec);                                    \
@@ -565,27 +601,34 @@ static bool pick_tiled_form(const Config& c, int vrec, bool xpose, KernelInfo& k
   return false;
 }
 
-template <typename T, int D>
+template <typename T, int D, int GEOM>
 static bool pick_tiled_nq(const Config& c, int lb, int vrec, bool xpose, KernelInfo& k) {
-  if (c.n_q == 1) return lb == 1 ? pick_tiled_form<T, D, 1, 1>(c, vrec, xpose, k)
-                                 : pick_tiled_form<T, D, 1, 2>(c, vrec, xpose, k);
-  if (c.n_q == 2) return lb == 1 ? pick_tiled_form<T, D, 2, 1>(c, vrec, true, k)
-                                 : pick_tiled_form<T, D, 2, 2>(c, vrec, true, k);
+  if (c.n_q == 1) return lb == 1 ? pick_tiled_form<T, D, 1, 1, GEOM>(c, vrec, xpose, k)
+                                 : pick_tiled_form<T, D, 1, 2, GEOM>(c, vrec, xpose, k);
+  if (c.n_q == 2) return lb == 1 ? pick_tiled_form<T, D, 2, 1, GEOM>(c, vrec, true, k)
+                                 : pick_tiled_form<T, D, 2, 2, GEOM>(c, vrec, true, k);
   return false;
 }
 
-static bool pick_tiled_kernel(const Config& c, int lb, int vrec, KernelInfo& k) {
-  const bool xpose = env_int("TXB_TILED_XPOSE", 0) != 0;
+template <int GEOM>
+static bool pick_tiled_geom(const Config& c, int lb, int vrec, bool xpose, KernelInfo& k) {
   if (c.dtype == 4)
-    return c.dim == 2 ? pick_tiled_nq<float, 2>(c, lb, vrec, xpose, k) : pick_tiled_nq<float, 3>(c, lb, vrec, xpose, k);
-  return c.dim == 2 ? pick_tiled_nq<double, 2>(c, lb, vrec, xpose, k) : pick_tiled_nq<double, 3>(c, lb, vrec, xpose, k);
+    return c.dim == 2 ? pick_tiled_nq<float, 2, GEOM>(c, lb, vrec, xpose, k)
+                      : pick_tiled_nq<float, 3, GEOM>(c, lb, vrec, xpose, k);
+  return c.dim == 2 ? pick_tiled_nq<double, 2, GEOM>(c, lb, vrec, xpose, k)
+                    : pick_tiled_nq<double, 3, GEOM>(c, lb, vrec, xpose, k);
+}
+
+static bool pick_tiled_kernel(const Config& c, int lb, int vrec, bool geom, KernelInfo& k) {
+  const bool xpose = env_int("TXB_TILED_XPOSE", 0) != 0;
+  return geom ? pick_tiled_geom<1>(c, lb, vrec, xpose, k) : pick_tiled_geom<0>(c, lb, vrec, xpose, k);
 }
 
 template <typename T>
 static int launch_tiled(const Config& c, const KernelInfo& k, Geometry g, int64_t n_cells, const void* basis,
                         const void* basis_der, const void* weights, const double* vertices, const int32_t* records,
-                        const void* local, int vrec, const void* coeffs_global, const void* aux, void* out,
-                        int64_t* bad_cell, cudaStream_t stream) {
+                        const void* local, int vrec, const void* coeffs_global, const void* inv_j,
+                        const void* det_j, const void* aux, void* out, int64_t* bad_cell, cudaStream_t stream) {
   TiledArgs<T> a;
   a.n_cells = n_cells;
   // static chunks must start on tile boundaries
@@ -611,6 +654,9 @@ static int launch_tiled(const Config& c, const KernelInfo& k, Geometry g, int64_
   a.vrec = vrec;
   auto al16 = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
   a.aux_bulk = c.aux != 0 && al16(aux) && env_int("TXB_DISABLE_BULK", 0) == 0;
+  a.inv_j = (const T*)inv_j;
+  a.det_j = (const T*)det_j;
+  a.geom_bulk = inv_j && al16(inv_j) && al16(det_j) && env_int("TXB_DISABLE_BULK", 0) == 0;
   a.out_vec = al16(out);
   a.sleep_ns = (uint32_t)std::max(0, env_int("TXB_TILED_SLEEP_NS", 0));
   a.consumer_sleep_ns = (uint32_t)std::max(0, env_int("TXB_TILED_CONSUMER_SLEEP_NS", 20000));  // measured +2 %
@@ -694,8 +740,9 @@ extern "C" int txb_integrate_mesh_tiled(int form_code, int aux_mode, int dtype_b
                                         int64_t n_cells, int64_t n_vertices, const void* basis,
                                         const void* basis_der, const void* weights, const double* vertices,
                                         int tile_cells, const int32_t* records, int vrec, const void* local,
-                                        int local_bytes, const void* coeffs_global, const void* aux, void* out,
-                                        int64_t* bad_cell, void* stream) {
+                                        int local_bytes, const void* coeffs_global, const void* inv_j,
+                                        const void* det_j, const void* aux, void* out, int64_t* bad_cell,
+                                        void* stream) {
   Config c{form_code, aux_mode, dtype_bytes, dim, n_q, n_comp};
   int rc = validate(c);
   if (rc) return rc;
@@ -721,8 +768,13 @@ extern "C" int txb_integrate_mesh_tiled(int form_code, int aux_mode, int dtype_b
     set_error("tiles: local_bytes 1|2 and vrec a multiple of 4 >= 8 (got %d, %d)", local_bytes, vrec);
     return TXB_E_ARG;
   }
+  if ((inv_j == nullptr) != (det_j == nullptr)) {
+    set_error("give both inv_j and det_j, or neither (computed from the vertices)");
+    return TXB_E_ARG;
+  }
+  const bool geom = inv_j != nullptr;
   KernelInfo k;
-  if (!pick_tiled_kernel(c, local_bytes, vrec, k)) {
+  if (!pick_tiled_kernel(c, local_bytes, vrec, geom, k)) {
     set_error("no tiled kernel instantiation for this configuration");
     return TXB_E_UNSUPPORTED;
   }
@@ -731,7 +783,7 @@ extern "C" int txb_integrate_mesh_tiled(int form_code, int aux_mode, int dtype_b
   if (rc) return rc;
   if (n_cells == 0) return TXB_OK;
   auto al16 = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
-  if (!vertices || !records || !local || !coeffs_global || !out || (c.aux != 0 && !aux)) {
+  if ((!geom && !vertices) || !records || !local || !coeffs_global || !out || (c.aux != 0 && !aux)) {
     set_error("NULL device pointer");
     return TXB_E_ARG;
   }
@@ -741,7 +793,7 @@ extern "C" int txb_integrate_mesh_tiled(int form_code, int aux_mode, int dtype_b
   }
   if (dtype_bytes == 4)
     return launch_tiled<float>(c, k, g, n_cells, basis, basis_der, weights, vertices, records, local, vrec,
-                               coeffs_global, aux, out, bad_cell, (cudaStream_t)stream);
+                               coeffs_global, inv_j, det_j, aux, out, bad_cell, (cudaStream_t)stream);
   return launch_tiled<double>(c, k, g, n_cells, basis, basis_der, weights, vertices, records, local, vrec,
-                              coeffs_global, aux, out, bad_cell, (cudaStream_t)stream);
+                              coeffs_global, inv_j, det_j, aux, out, bad_cell, (cudaStream_t)stream);
 }

@@ -555,15 +555,15 @@ def integrate_mesh(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: Quadr
     B, D, W = (np.ascontiguousarray(x, dtype=dt) for x in (tab.basis, tab.basis_der, rule.weights))
     ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
     tiles = None
-    if cell_geom is None and n > 0 and _tiled_enabled(mesh, rule):
+    if n > 0 and _tiled_enabled(mesh, rule):
         tiles = cell_tiles(C, mesh.dim, default_tile_cells(mesh.dim, rule.n_q))
     if tiles is not None:
-        # geometry + gather from per-tile vertex tables (csrc/txb_integrate_tiled.cu)
+        # (geometry +) gather from per-tile vertex tables (csrc/txb_integrate_tiled.cu)
         rc = _lib.lib().txb_integrate_mesh_tiled(
             kernel[0], kernel[1], dt.itemsize, mesh.dim, rule.n_q, form.n_comp, n, mesh.n_vertices,
             B.ctypes.data, D.ctypes.data, W.ctypes.data, X.data_ptr(), tiles.tile_cells, tiles.records.data_ptr(),
-            tiles.vrec, tiles.local.data_ptr(), tiles.local_bytes, g.data_ptr(), ptr(av), res.data_ptr(), ptr(bad),
-            _stream_ptr(torch))
+            tiles.vrec, tiles.local.data_ptr(), tiles.local_bytes, g.data_ptr(), ptr(inv), ptr(det), ptr(av),
+            res.data_ptr(), ptr(bad), _stream_ptr(torch))
         _lib.check(rc, "txb_integrate_mesh_tiled")
     else:
         rc = _lib.lib().txb_integrate_mesh(

@@ -186,10 +186,13 @@ def test_fused_mesh_kernel_unaligned_connectivity():
 @pytest.mark.parametrize("dim", [2, 3])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 @pytest.mark.parametrize("offset", [0, 1])
-def test_fused_mesh_kernel_elasticity_coefficient_alignment(dim, dtype, offset):
+@pytest.mark.parametrize("tiled", ["0", "1"])
+def test_fused_mesh_kernel_elasticity_coefficient_alignment(dim, dtype, offset, tiled, monkeypatch):
     """Given geometry, elasticity: the coefficient gathers pair a vertex's
     components (16/8-byte loads, even and odd vertices) when the global vector
-    is pair-aligned, scalar loads when it is not — same bits either way."""
+    is pair-aligned, scalar loads when it is not — same bits either way (and
+    through the tiled kernel, TXB_TILED=1, whose gatherer copies scalars)."""
+    monkeypatch.setenv("TXB_TILED", tiled)
     mesh, form, glob, aux = _mesh_problem(dim, 6 if dim == 3 else 20, txb.elasticity_form, None, seed=21 + dim)
     rule = txb.quadrature_rule(dim, 1)
     npdt = np.float64 if dtype == "f64" else np.float32

@@ -85,12 +85,17 @@ def test_tiled_bitwise_vs_oracle_and_per_cell_kernel(dim, n, shuffle, n_cells, f
         for dtype, npdt in (("f64", np.float64), ("f32", np.float32)):
             ref = _oracle(mesh, form, glob, aux, rule, npdt)
             g = torch.from_numpy(glob.astype(npdt)).cuda()
-            outs = {}
+            inv, det = oracle.geometry(mesh.vertices, mesh.cells)
+            geom = txb.CellGeometry(inv.astype(npdt), det.astype(npdt))
             for mode in ("tiled", "tiled_xpose", "per_cell"):
                 monkeypatch.setenv("TXB_TILED", "0" if mode == "per_cell" else "1")
                 monkeypatch.setenv("TXB_TILED_XPOSE", "1" if mode == "tiled_xpose" else "0")
-                outs[mode] = txb.integrate_mesh(mesh, layout, tab, rule, form, g, aux, dtype=dtype).cpu().numpy()
-                assert bitwise_equal(outs[mode], ref), (mode, dtype, rule.n_q)
+                out = txb.integrate_mesh(mesh, layout, tab, rule, form, g, aux, dtype=dtype).cpu().numpy()
+                assert bitwise_equal(out, ref), (mode, dtype, rule.n_q)
+                # given geometry (cast once to the run precision, as executor.py:77-90): the same bits
+                out = txb.integrate_mesh(mesh, layout, tab, rule, form, g, aux, dtype=dtype,
+                                         cell_geom=geom).cpu().numpy()
+                assert bitwise_equal(out, ref), (mode, dtype, rule.n_q, "given geometry")
 
 
 @pytest.mark.parametrize("tile", ["64", "96", "192", "256"])
@@ -111,6 +116,28 @@ def test_tiled_tile_sizes(tile, monkeypatch):
         else:
             with pytest.raises(txb.ConfigurationError):
                 txb.integrate_mesh(mesh, txb.FieldLayout(1), tab, rule, form, g, aux, dtype="f64")
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_tiled_given_geometry_unaligned(dtype):
+    """Given geometry whose bases are off 16 bytes (read from global memory,
+    not bulk-copied): same bits as the oracle."""
+    npdt = np.float64 if dtype == "f64" else np.float32
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    for dim in (2, 3):
+        mesh, form, glob, aux = _problem(dim, 7 if dim == 3 else 25, txb.poisson_varcoef_form, "p0", seed=13)
+        rule = txb.quadrature_rule(dim, 1)
+        tab = txb.tabulate(dim, rule)
+        ref = _oracle(mesh, form, glob, aux, rule, npdt)
+        inv, det = oracle.geometry(mesh.vertices, mesh.cells)
+        bi = torch.empty(inv.size + 1, dtype=tdt, device="cuda")
+        bd = torch.empty(det.size + 1, dtype=tdt, device="cuda")
+        gi, gd = bi[1:].view(inv.shape), bd[1:].view(det.shape)
+        gi.copy_(torch.from_numpy(inv.astype(npdt)))
+        gd.copy_(torch.from_numpy(det.astype(npdt)))
+        out = txb.integrate_mesh(mesh, txb.FieldLayout(1), tab, rule, form, torch.from_numpy(glob.astype(npdt)).cuda(),
+                                 aux, dtype=dtype, cell_geom=txb.CellGeometry(gi, gd))
+        assert bitwise_equal(out.cpu().numpy(), ref), dim
 
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])

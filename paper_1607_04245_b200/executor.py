@@ -191,14 +191,23 @@ def invalidate_mesh_cache() -> None:
     _MESH_CACHE.clear()
     _PART_CACHE.clear()
     _TILE_CACHE.clear()
+    _ORIENTED.clear()
+
+
+_FP_ROWS: dict = {}
 
 
 def _fingerprint(a: np.ndarray) -> bytes:
     rows = a.shape[0]
     if rows == 0:
         return b""
-    idx = np.unique(np.linspace(0, rows - 1, min(rows, 64)).astype(np.int64))
-    return np.ascontiguousarray(a[idx]).tobytes()
+    idx = _FP_ROWS.get(rows)
+    if idx is None:  # the 64 sampled rows of an array of this length (memoised: per-call host cost)
+        idx = np.unique(np.linspace(0, rows - 1, min(rows, 64)).astype(np.int64))
+        if len(_FP_ROWS) > 256:
+            _FP_ROWS.clear()
+        _FP_ROWS[rows] = idx
+    return a[idx].tobytes()
 
 
 def _device_index(torch) -> int:
@@ -238,8 +247,16 @@ def _mesh_on_device(mesh: Mesh, torch):
     cells = torch.from_numpy(np.ascontiguousarray(mesh.cells, dtype=np.int64)).to("cuda")
     verts = torch.from_numpy(np.ascontiguousarray(mesh.vertices, dtype=np.float64)).to("cuda")
     _MESH_CACHE.clear()
+    _ORIENTED.clear()
     _MESH_CACHE[key] = (mesh.cells, mesh.vertices, cells, verts)
     return cells, verts
+
+
+# Device meshes (id of the cached connectivity tensor) whose orientation was
+# verified (every detJ > 0) by a checked call: their later residuals skip the
+# flag read-back, so a device-resident call stays asynchronous.  Cleared with
+# the mesh cache (a new upload is checked again).
+_ORIENTED: set = set()
 
 
 _PART_CACHE: dict = {}
@@ -293,14 +310,20 @@ def integrate_transposed(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule:
     glob_dev = _dev(glob, torch, dt)
     aux_dev = None if aux is None else CellAux(aux.space, _dev(aux.values, torch, dt))
 
+    # the orientation of an uploaded mesh is checked once (one host sync), not per residual
+    verified = id(cells_dev) in _ORIENTED
+    check = check_orientation and not verified
     if _mesh_fusable(tab, rule) and not isinstance(kernel, _backend.JitKernel):
-        # geometry + gather + cast + integrate in one kernel (csrc/txb_integrate_mesh.cu)
+        # geometry + gather + cast + integrate in one kernel (csrc/txb_integrate_tiled.cu / _mesh.cu)
         elem = integrate_mesh(mesh, layout, tab, rule, form, glob_dev, aux_dev, dtype=dt, cell_geom=cell_geom,
-                              cells=cells_dev, vertices=verts_dev, n_bl=n_bl, check_orientation=check_orientation)
+                              cells=cells_dev, vertices=verts_dev, n_bl=n_bl, check_orientation=check)
+        if check and cell_geom is None:
+            _ORIENTED.add(id(cells_dev))
     elif isinstance(kernel, _backend.JitKernel) and cell_geom is None and os.environ.get("TXB_JIT_MESH", "1") != "0":
         # run-time compiled form, fused the same way (csrc/txb_jit_kernel.cuh, mesh entry points)
-        elem = _jit_mesh(kernel, mesh, tab, rule, form, glob_dev, aux_dev, dt, cells_dev, verts_dev, n_bl,
-                         check_orientation)
+        elem = _jit_mesh(kernel, mesh, tab, rule, form, glob_dev, aux_dev, dt, cells_dev, verts_dev, n_bl, check)
+        if check:
+            _ORIENTED.add(id(cells_dev))
     else:
         if cell_geom is None:
             cell_geom = compute_geometry(mesh, cells=cells_dev, vertices=verts_dev, device_out=True)
@@ -314,7 +337,7 @@ def integrate_transposed(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule:
         # integrate_reference), so the f32 residual equals the reference's bits
         span = geom.n_chunks * geom.n_chunk
         elem[span:] = _remainder_f64(mesh, layout, tab, rule, form, kernel, glob, aux, cell_geom, cells_dev,
-                                     verts_dev, span, n_bl, check_orientation).to(elem.dtype)
+                                     verts_dev, span, n_bl, check).to(elem.dtype)
     residual = scatter_add_element_vectors(mesh, layout, elem, incidence=_incidence_for(mesh, cells_dev))
 
     trace = ExecutionTrace.uniform(geom, dt.itemsize, model_batch_counters(geom, form, dt.itemsize, aux),

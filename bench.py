@@ -810,11 +810,15 @@ def variant_rows(peak, steps):
             k = variant_steps(vw["n"], steps)
             tot, _ = time_device(vw, k, 5, ns)
             vl = tot / k
-            return [{"config": v, "dtype": vw["dtype"], "cells": vw["n"], "steps": k, "sets": ns,
-                     "gflops": vf * vw["n"] / (vl * 1e-3) / 1e9,
-                     "gbs_launch": vb * vw["n"] / (vl * 1e-3) / 1e9,
-                     "frac": vb * vw["n"] / (vl * 1e-3) / 1e9 / peak, "launch_ms": vl,
-                     "bytes_per_cell": vb}]
+            row = {"config": v, "dtype": vw["dtype"], "cells": vw["n"], "steps": k, "sets": ns,
+                   "gflops": vf * vw["n"] / (vl * 1e-3) / 1e9,
+                   "gbs_launch": vb * vw["n"] / (vl * 1e-3) / 1e9,
+                   "frac": vb * vw["n"] / (vl * 1e-3) / 1e9 / peak, "launch_ms": vl,
+                   "bytes_per_cell": vb}
+            if vw["n"] <= (1 << 16):
+                row["note"] = ("launch-latency bound (6 MB per launch): a plain copy kernel moving the same bytes "
+                               "takes 3.5 us per chained launch, profiles/r1f_scan.md")
+            return [row]
         _guarded(rows, v, one)
     return rows
 

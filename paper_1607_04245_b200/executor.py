@@ -155,6 +155,21 @@ def integrate_reference(tab: Tabulation, rule: QuadratureRule, geom: CellGeometr
     return integrate_cells(tab, rule, geom, coeffs, aux, form, dtype="f64")
 
 
+def _kernel_decomposition(n_bl: int, n_cb: int):
+    """(N_bl, N_cb) handed to the kernels by the reference-API calls.  The
+    caller's decomposition shapes the execution geometry, its checks
+    (ConfigurationError, CapacityError) and the modelled trace exactly as in
+    the reference; the device schedule does not change a single bit of the
+    result (tests/test_gpu_parity.py decomposition grid), so by default the
+    kernels run their B200-tuned batches with dynamic scheduling -- the
+    reference's own defaults (N_bl 16, N_cb 8: 64-cell batches in static
+    8-batch chunks) cost 1.2-3x on this device (tools/ncb_probe.py).
+    TXB_PAPER_DECOMPOSITION=1 launches the requested decomposition as is."""
+    if os.environ.get("TXB_PAPER_DECOMPOSITION", "0") != "0":
+        return n_bl, n_cb
+    return 0, 0
+
+
 def execute_chunk(geom: ExecutionGeometry, tab: Tabulation, rule: QuadratureRule, cell_geom: CellGeometry,
                   coeffs, aux: Optional[CellAux], form: PhysicsForm, *, dtype="f64", chunk_index: int = 0,
                   shared_mem_limit: Optional[int] = DEFAULT_SHARED_MEM_LIMIT, log_tasks: bool = False,
@@ -168,7 +183,8 @@ def execute_chunk(geom: ExecutionGeometry, tab: Tabulation, rule: QuadratureRule
     if log_tasks:
         raise ValueError("log_tasks is a simulated-device audit feature; not available on the cuda lane")
     _resolve_backend(backend, form, geom.n_q, aux, dt.itemsize)
-    elem = integrate_cells(tab, rule, cell_geom, coeffs, aux, form, dtype=dt, n_bl=geom.n_bl, n_cb=geom.n_cb)
+    k_bl, k_cb = _kernel_decomposition(geom.n_bl, geom.n_cb)
+    elem = integrate_cells(tab, rule, cell_geom, coeffs, aux, form, dtype=dt, n_bl=k_bl, n_cb=k_cb)
     per_batch = model_batch_counters(geom, form, dt.itemsize, aux)
     trace = ChunkTrace(chunk_index=chunk_index, batches=[replace(per_batch) for _ in range(geom.n_cb)])
     return elem, trace
@@ -303,6 +319,7 @@ def integrate_transposed(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule:
     kernel = _resolve_backend(backend, form, rule.n_q, aux, dt.itemsize)
     if aux is not None and int(aux.values.shape[0]) != mesh.n_cells:
         raise ShapeError(f"auxiliary data covers {aux.values.shape[0]} cells, expected {mesh.n_cells}")
+    n_bl, n_cb = _kernel_decomposition(n_bl, n_cb)  # (geom above keeps the caller's decomposition)
     torch = _torch()
     host_out = isinstance(coeffs_global, np.ndarray) or not hasattr(coeffs_global, "is_cuda")
     cells_dev, verts_dev = _mesh_on_device(mesh, torch)

@@ -143,3 +143,22 @@ def test_integrate_transposed_orientation_error_names_the_cell():
     with pytest.raises(txb.OrientationError, match="cell 2"):
         txb.integrate_transposed(mesh, txb.FieldLayout(1), txb.tabulate(3, rule), rule, txb.poisson_form(3),
                                  np.ones(6), None, n_bl=4, n_cb=2, shared_mem_limit=None)
+
+
+@pytest.mark.parametrize("paper", ["0", "1"])
+def test_reference_decomposition_is_a_model_parameter(paper, monkeypatch):
+    """The caller's (N_bl, N_cb) shape the geometry, checks and trace; the
+    device runs its tuned schedule unless TXB_PAPER_DECOMPOSITION=1 -- the
+    element vectors and the residual are the same bits either way."""
+    monkeypatch.setenv("TXB_PAPER_DECOMPOSITION", paper)
+    form, mesh, layout, rule, tab, geom, coeffs = make_problem(3, txb.poisson_varcoef_form, 5)
+    kappa = txb.CellAux("p0", np.random.default_rng(3).uniform(0.5, 1.5, (mesh.n_cells, 1)))
+    glob = np.random.default_rng(4).standard_normal(mesh.n_vertices)
+    res, trace = txb.integrate_transposed(mesh, layout, tab, rule, form, glob, kappa, n_bl=16, n_cb=8,
+                                          dtype="f64", shared_mem_limit=None)
+    g = txb.derive_execution_geometry(3, 4, 1, 1, 16, 8, mesh.n_cells)
+    assert trace.remainder_cells == g.n_r
+    inv, det = oracle.geometry(mesh.vertices, mesh.cells)
+    elem = oracle.integrate(1, 1, tab.basis, tab.basis_der, rule.weights, inv, det,
+                            oracle.gather(mesh.cells, glob, 1), kappa.values)
+    assert bitwise_equal(res, oracle.scatter_add(mesh.cells, elem, mesh.n_vertices))

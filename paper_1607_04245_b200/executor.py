@@ -24,6 +24,7 @@ Differences from the reference, all deliberate:
 from __future__ import annotations
 
 import os
+import weakref
 from dataclasses import replace
 from typing import Optional, Union
 
@@ -263,16 +264,23 @@ def _mesh_on_device(mesh: Mesh, torch):
     cells = torch.from_numpy(np.ascontiguousarray(mesh.cells, dtype=np.int64)).to("cuda")
     verts = torch.from_numpy(np.ascontiguousarray(mesh.vertices, dtype=np.float64)).to("cuda")
     _MESH_CACHE.clear()
-    _ORIENTED.clear()
     _MESH_CACHE[key] = (mesh.cells, mesh.vertices, cells, verts)
     return cells, verts
 
 
-# Device meshes (id of the cached connectivity tensor) whose orientation was
-# verified (every detJ > 0) by a checked call: their later residuals skip the
-# flag read-back, so a device-resident call stays asynchronous.  Cleared with
-# the mesh cache (a new upload is checked again).
-_ORIENTED: set = set()
+# Cached device connectivity tensors (weakly, by id) whose mesh passed the
+# orientation check (every detJ > 0) in a checked call: their later residuals
+# skip the flag read-back, so a device-resident call stays asynchronous.  An
+# entry dies with its tensor (a new upload is checked again).
+_ORIENTED = weakref.WeakValueDictionary()
+
+
+def _orientation_verified(cells_dev) -> bool:
+    return _ORIENTED.get(id(cells_dev)) is cells_dev
+
+
+def _mark_oriented(cells_dev) -> None:
+    _ORIENTED[id(cells_dev)] = cells_dev
 
 
 _PART_CACHE: dict = {}
@@ -328,19 +336,18 @@ def integrate_transposed(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule:
     aux_dev = None if aux is None else CellAux(aux.space, _dev(aux.values, torch, dt))
 
     # the orientation of an uploaded mesh is checked once (one host sync), not per residual
-    verified = id(cells_dev) in _ORIENTED
-    check = check_orientation and not verified
+    check = check_orientation and not _orientation_verified(cells_dev)
     if _mesh_fusable(tab, rule) and not isinstance(kernel, _backend.JitKernel):
         # geometry + gather + cast + integrate in one kernel (csrc/txb_integrate_tiled.cu / _mesh.cu)
         elem = integrate_mesh(mesh, layout, tab, rule, form, glob_dev, aux_dev, dtype=dt, cell_geom=cell_geom,
                               cells=cells_dev, vertices=verts_dev, n_bl=n_bl, check_orientation=check)
         if check and cell_geom is None:
-            _ORIENTED.add(id(cells_dev))
+            _mark_oriented(cells_dev)
     elif isinstance(kernel, _backend.JitKernel) and cell_geom is None and os.environ.get("TXB_JIT_MESH", "1") != "0":
         # run-time compiled form, fused the same way (csrc/txb_jit_kernel.cuh, mesh entry points)
         elem = _jit_mesh(kernel, mesh, tab, rule, form, glob_dev, aux_dev, dt, cells_dev, verts_dev, n_bl, check)
         if check:
-            _ORIENTED.add(id(cells_dev))
+            _mark_oriented(cells_dev)
     else:
         if cell_geom is None:
             cell_geom = compute_geometry(mesh, cells=cells_dev, vertices=verts_dev, device_out=True)
@@ -744,8 +751,12 @@ def integrate_partitioned(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule
         aux_dev = None if aux is None else CellAux(aux.space, _dev(aux.values[lo:hi], torch, dt))
         cells_dev, verts_dev = _partition_on_device(mesh, lo, hi, torch)
         if _mesh_fusable(tab, rule) and not isinstance(kernel, _backend.JitKernel):
+            # orientation checked on the first residual of this uploaded range only (one host sync)
+            check_o = not _orientation_verified(cells_dev)
             integrate_mesh(sub, layout, tab, rule, form, glob_dev, aux_dev, dtype=dt, cells=cells_dev,
-                           vertices=verts_dev, out=elem, n_bl=n_bl)
+                           vertices=verts_dev, out=elem, n_bl=n_bl, check_orientation=check_o)
+            if check_o:
+                _mark_oriented(cells_dev)
         else:
             g = compute_geometry(sub, cells=cells_dev, vertices=verts_dev, device_out=True)
             blocks = gather_coefficients(sub, layout, glob_dev, cells=cells_dev)

@@ -530,10 +530,12 @@ def cell_tiles(cells_dev, dim: int, tile_cells: int) -> CellTiles:
     """The CellTiles of a device connectivity tensor, built once per (memory
     range, tile size, device) and cached (the tensor is kept alive with them,
     so the address cannot be reused; a view of the same range hits the same
-    entry).  The tensor must not be modified in place -- the mesh caches above
-    hand out fresh tensors when the host mesh changes."""
+    entry).  An in-place modification through torch bumps the tensor's version
+    and rebuilds the tables; writes through raw pointers are not seen (the
+    mesh caches above hand out fresh tensors when the host mesh changes)."""
+    # (torch's in-place version counter: a connectivity tensor modified in place by torch ops misses)
     key = (cells_dev.data_ptr(), tuple(cells_dev.shape), tuple(cells_dev.stride()), cells_dev.device.index,
-           tile_cells)
+           tile_cells, cells_dev._version)
     hit = _TILE_CACHE.get(key)
     if hit is not None:  # (the cached tensor keeps that memory alive: same key, same storage; views match too)
         return hit[1]

@@ -252,3 +252,20 @@ def test_tile_builder_rejects_out_of_range_ids():
     cells = torch.tensor([[0, 1, 2, -1]], dtype=torch.int64, device="cuda")
     with pytest.raises(IndexError):
         executor.CellTiles(cells, 3, 128)
+
+
+def test_tiles_rebuilt_after_in_place_modification():
+    """Tables are cached per connectivity tensor; an in-place change through
+    torch (version counter) rebuilds them, so the result follows the new cells."""
+    mesh, form, glob, aux = _problem(3, 5, txb.poisson_varcoef_form, "p0", seed=5)
+    rule = txb.quadrature_rule(3, 1)
+    tab = txb.tabulate(3, rule)
+    cells = torch.from_numpy(mesh.cells).cuda()
+    g = torch.from_numpy(glob).cuda()
+    txb.integrate_mesh(mesh, txb.FieldLayout(1), tab, rule, form, g, aux, cells=cells)
+    flipped = mesh.cells.copy()
+    flipped[:, [1, 2]] = flipped[:, [2, 1]]  # every cell negatively oriented now
+    cells.copy_(torch.from_numpy(flipped))
+    with pytest.raises(txb.OrientationError):
+        txb.integrate_mesh(txb.Mesh(3, mesh.vertices, flipped), txb.FieldLayout(1), tab, rule, form, g, aux,
+                           cells=cells)

@@ -18,7 +18,10 @@ Differences from the reference, all deliberate:
     the reference's bit for bit (tests/test_residual_golden.py);
   * ``jobs`` is accepted and has no effect on the result -- the reference's
     thread pool over chunks (executor.py:228-239) produces the same bits as
-    its single call, and here one launch covers every chunk.
+    its single call, and here one launch covers every chunk;
+  * the caller's (N_bl, N_cb) define the execution geometry, its checks and
+    the modelled trace exactly as in the reference, while the kernels run
+    their B200-tuned batches (the same bits; _kernel_decomposition).
 """
 
 from __future__ import annotations

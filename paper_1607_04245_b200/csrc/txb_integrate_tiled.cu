@@ -181,7 +181,6 @@ struct TiledArgs {
   int aux_bulk;                // aux base 16-byte aligned: full batches' aux slices arrive by bulk copy
   int geom_bulk;               // GEOM == 1: inv_j / det_j bases 16-byte aligned (bulk copies, else global loads)
   int out_vec;                 // out base 16-byte aligned: in-lane rows stored with vector stores
-  uint32_t sleep_ns;           // producer / gatherer try_wait suspend hint (0: plain retry)
   uint32_t consumer_sleep_ns;  // consumer `ready` try_wait suspend hint (0: plain retry)
   Tabulation<T> tab;
 };
@@ -474,7 +473,7 @@ integrate_tiled_kernel(const __grid_constant__ TiledArgs<T> a) {
       }
       bulk_g2s(st + L::rec_off(nbc), a.records + (c0 / nbc) * vrec, rb, bar, policy);
       return true;
-    }, a.sleep_ns);
+    });
     return;
   }
 
@@ -483,10 +482,7 @@ integrate_tiled_kernel(const __grid_constant__ TiledArgs<T> a) {
     int stage = 0;
     uint32_t phase = 0;
     for (;;) {
-      if (a.sleep_ns)
-        mbar_wait_sleep(&p.full[stage], phase, a.sleep_ns);
-      else
-        mbar_wait(&p.full[stage], phase);
+      mbar_wait(&p.full[stage], phase);
       const int n = p.info_n[stage];
       if (n != 0) {
         unsigned char* st = smem + stage * stage_bytes;
@@ -658,7 +654,6 @@ static int launch_tiled(const Config& c, const KernelInfo& k, Geometry g, int64_
   a.det_j = (const T*)det_j;
   a.geom_bulk = inv_j && al16(inv_j) && al16(det_j) && env_int("TXB_DISABLE_BULK", 0) == 0;
   a.out_vec = al16(out);
-  a.sleep_ns = (uint32_t)std::max(0, env_int("TXB_TILED_SLEEP_NS", 0));
   a.consumer_sleep_ns = (uint32_t)std::max(0, env_int("TXB_TILED_CONSUMER_SLEEP_NS", 20000));  // measured +2 %
   fill_tab(a.tab, c.n_q, c.dim + 1, c.dim, basis, basis_der, weights);
   void* params[] = {&a};

@@ -241,15 +241,12 @@ __device__ __forceinline__ void pipeline_wait_prior_grid() {
 
 template <class Args, class Issue>
 __device__ __forceinline__ void pipeline_produce(const Args& a, const PipelineSmem& p, unsigned char* stages,
-                                                 int stage_bytes, Issue issue, uint32_t sleep_ns = 0) {
+                                                 int stage_bytes, Issue issue) {
   const int nbc = a.n_bc;
   int stage = 0;
   uint32_t phase = 0;
   auto publish = [&](int64_t c0, int ncell) {
-    if (sleep_ns)
-      mbar_wait_sleep(&p.empty[stage], phase ^ 1, sleep_ns);
-    else
-      mbar_wait(&p.empty[stage], phase ^ 1);
+    mbar_wait(&p.empty[stage], phase ^ 1);
     p.info_c0[stage] = c0;
     p.info_n[stage] = ncell;  // 0 = stop
     if (ncell == 0 || !issue(stages + stage * stage_bytes, c0, ncell, &p.full[stage])) {

@@ -422,7 +422,7 @@ def _check_aux_shape(aux, n_cells: int, n_b: int, form: PhysicsForm):
 
 
 def _jit_mesh(kernel, mesh: Mesh, tab: Tabulation, rule: QuadratureRule, form: PhysicsForm, glob_dev, aux_dev, dt,
-              cells_dev, verts_dev, n_bl: int, check_orientation: bool = True):
+              cells_dev, verts_dev, n_bl: int, check_orientation: bool = True, out=None):
     """Element vectors of a run-time compiled form straight from the mesh
     (txb_jit_integrate_mesh: float64 geometry + gather in-kernel, any
     tabulation).  Raises OrientationError for a cell with detJ <= 0."""
@@ -436,7 +436,7 @@ def _jit_mesh(kernel, mesh: Mesh, tab: Tabulation, rule: QuadratureRule, form: P
     _check_aux_shape(aux_dev, n, tab.n_b, form)
     if int(glob_dev.numel()) != mesh.n_vertices * form.n_comp:
         raise ShapeError(f"global vector has {glob_dev.numel()} entries, expected {mesh.n_vertices * form.n_comp}")
-    res = torch.empty((n, tab.n_b, form.n_comp), dtype=glob_dev.dtype, device="cuda")
+    res = out if out is not None else torch.empty((n, tab.n_b, form.n_comp), dtype=glob_dev.dtype, device="cuda")
     bad = torch.full((1,), -1, dtype=torch.int64, device="cuda") if check_orientation else None
     B, D, W = (np.ascontiguousarray(x, dtype=dt) for x in (tab.basis, tab.basis_der, rule.weights))
     av = None if aux_dev is None else aux_dev.values.contiguous()
@@ -760,6 +760,13 @@ def integrate_partitioned(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule
             check_o = not _orientation_verified(cells_dev)
             integrate_mesh(sub, layout, tab, rule, form, glob_dev, aux_dev, dtype=dt, cells=cells_dev,
                            vertices=verts_dev, out=elem, n_bl=n_bl, check_orientation=check_o)
+            if check_o:
+                _mark_oriented(cells_dev)
+        elif isinstance(kernel, _backend.JitKernel) and os.environ.get("TXB_JIT_MESH", "1") != "0":
+            # run-time compiled form: its (tiled) mesh entry point, as integrate_transposed
+            check_o = not _orientation_verified(cells_dev)
+            _jit_mesh(kernel, sub, tab, rule, form, glob_dev, aux_dev, dt, cells_dev, verts_dev, n_bl, check_o,
+                      out=elem)
             if check_o:
                 _mark_oriented(cells_dev)
         else:

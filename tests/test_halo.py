@@ -161,14 +161,18 @@ class Mailbox:
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("world,align", [(1, 256), (2, 256), (3, 64), (8, 16)])
-@pytest.mark.parametrize("physics", ["varcoef_p0", "elasticity"])
+@pytest.mark.parametrize("physics", ["varcoef_p0", "elasticity", "user_elastic_body"])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 def test_partitioned_integration_equals_reference_residual(world, align, physics, dtype):
     import paper_1607_04245_b200 as txb
+    from oracle import user_forms
 
     dim = 3
     mesh = txb.generate_unit_simplex_mesh(dim, 9)
-    form = txb.poisson_varcoef_form(dim) if physics == "varcoef_p0" else txb.elasticity_form(dim)
+    if physics == "user_elastic_body":  # a run-time compiled form (f0, P0 field): its tiled mesh entry point
+        form = user_forms.make_form(txb.user_form, "elastic_body", dim)
+    else:
+        form = txb.poisson_varcoef_form(dim) if physics == "varcoef_p0" else txb.elasticity_form(dim)
     layout = txb.FieldLayout(form.n_comp)
     rule = txb.quadrature_rule(dim, 1)
     tab = txb.tabulate(dim, rule)
@@ -189,9 +193,14 @@ def test_partitioned_integration_equals_reference_residual(world, align, physics
     # reference: every cell integrated, then np.add.at over the whole mesh (executor.py:266)
     inv, det = oracle.geometry(mesh.vertices, mesh.cells)
     co = oracle.gather(mesh.cells, glob, form.n_comp)
-    fc = 1 if physics == "varcoef_p0" else 2
-    elem = oracle.integrate(fc, 1 if aux is not None else 0, tab.basis, tab.basis_der, rule.weights, inv, det,
-                            co, None if aux is None else aux.values, npdt)
+    if physics == "user_elastic_body":
+        s = user_forms.spec("elastic_body", dim)
+        elem = oracle.integrate_forms(s["f1_many"], s["f0_many"], s["uses_grad_a"], s["aux"], tab.basis,
+                                      tab.basis_der, rule.weights, inv, det, co, aux.values, npdt)
+    else:
+        fc = 1 if physics == "varcoef_p0" else 2
+        elem = oracle.integrate(fc, 1 if aux is not None else 0, tab.basis, tab.basis_der, rule.weights, inv, det,
+                                co, None if aux is None else aux.values, npdt)
     want = oracle.scatter_add(mesh.cells, elem, mesh.n_vertices)
     assert bitwise_equal(got, want)
 

@@ -279,13 +279,15 @@ int txb_jit_integrate_mesh(void* kernel, int64_t n_cells, int64_t n_vertices, co
 
 /* The run-time compiled form over cell tiles (txb_tile_build tables), like
  * txb_integrate_mesh_tiled: each tile's distinct vertex rows gathered once
- * into shared memory.  n_q <= 2; tile_cells a multiple of (dim+1)*n_q and of
- * 32/n_q with at most 8 warp slices.  Same bits as txb_jit_integrate_mesh. */
+ * into shared memory; inv_j / det_j NULL (geometry in-kernel, same bits as
+ * txb_jit_integrate_mesh) or the caller's geometry in the kernel's precision
+ * (same bits as gather + txb_jit_integrate).  n_q <= 2; tile_cells a
+ * multiple of (dim+1)*n_q and of 32/n_q with at most 8 warp slices. */
 int txb_jit_integrate_mesh_tiled(void* kernel, int64_t n_cells, int64_t n_vertices, const void* basis,
                                  const void* basis_der, const void* weights, const double* vertices,
                                  int tile_cells, const int32_t* records, int vrec, const void* local,
-                                 int local_bytes, const void* coeffs_global, const void* aux, void* out,
-                                 int64_t* bad_cell, void* stream);
+                                 int local_bytes, const void* coeffs_global, const void* inv_j, const void* det_j,
+                                 const void* aux, void* out, int64_t* bad_cell, void* stream);
 
 /* ---- Halo exchange over peer memory (one node, NVLink / NVSwitch) --------
  * The global-residual exchange of halo.py without NCCL: every rank exposes a

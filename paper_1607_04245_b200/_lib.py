@@ -65,7 +65,7 @@ SIGNATURES = {
     "txb_jit_integrate": (_I, [_P, c_int64] + [_P] * 8 + [_I, _I, _P]),
     "txb_jit_integrate_mesh": (_I, [_P, c_int64, c_int64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P]),
     "txb_jit_integrate_mesh_tiled": (_I, [_P, c_int64, c_int64, _P, _P, _P, _P, _I, _P, _I, _P, _I, _P, _P, _P,
-                                          _P, _P]),
+                                          _P, _P, _P, _P]),
 }
 
 _lib = None

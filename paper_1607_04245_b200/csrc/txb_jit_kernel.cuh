@@ -69,10 +69,13 @@ struct MeshIn {
   const double* sx;
   const real* su;
   int vpitch, upitch, lb;
+  // tiled with the caller's geometry: the batch's inv_j / det_j rows (stage or global)
+  const real* g_inv;
+  const real* g_det;
 };
 
 // Where a slice's per-cell inputs come from.
-enum { SRC_CELLS = 0, SRC_MESH = 1, SRC_TILED = 2 };
+enum { SRC_CELLS = 0, SRC_MESH = 1, SRC_TILED = 2, SRC_TILED_GEOM = 3 };
 
 __device__ __forceinline__ int inv_bytes(int n) { return round_up(n * DD * S, 16); }
 __device__ __forceinline__ int det_bytes(int n) { return round_up(n * S, 16); }
@@ -99,7 +102,26 @@ __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const re
     real J[DD];
     real cf[NBC];
     real det;
-    if constexpr (MESH) {
+    if constexpr (SRC == SRC_TILED_GEOM) {
+      // coefficients from the tile's table, the caller's geometry as given (run precision)
+      int ids[NB];
+      if (mi.lb == 1) {
+        const uint32_t w = reinterpret_cast<const uint32_t*>(mi.s_local)[cell];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) ids[b] = (w >> (8 * b)) & 0xffu;
+      } else {
+        const uint2 w = reinterpret_cast<const uint2*>(mi.s_local)[cell];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) ids[b] = ((b < 2 ? w.x : w.y) >> (16 * (b & 1))) & 0xffffu;
+      }
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int c = 0; c < NCOMP; ++c) cf[b * NCOMP + c] = mi.su[c * mi.upitch + ids[b]];
+#pragma unroll
+      for (int i = 0; i < DD; ++i) J[i] = mi.g_inv[cell * DD + i];
+      det = mi.g_det[cell];
+    } else if constexpr (MESH) {
       // gather (mesh.py:202-217) and float64 geometry (mesh.py:150-190), cast once to the run
       // precision (executor.py:77-90): the reference's host steps, in-kernel
       double X[NB][D];
@@ -349,7 +371,7 @@ __device__ __forceinline__ void integrate_body(const IntegrateArgs<real>& a, con
   real* scratch = reinterpret_cast<real*>(scratch_base + warp * SCRATCH_BYTES);
   pipeline_consume(a, p, smem, stage_bytes, [&](const unsigned char* st, int64_t c0, int ncell) {
     real* out = a.out + c0 * NBC;
-    MeshIn mi{nullptr, nullptr, nullptr, nullptr, c0, nullptr, nullptr, nullptr, 0, 0, 0};
+    MeshIn mi{nullptr, nullptr, nullptr, nullptr, c0, nullptr, nullptr, nullptr, 0, 0, 0, nullptr, nullptr};
     if constexpr (MESH) {
       mi.ids = st ? reinterpret_cast<const int64_t*>(st) : m->cells + c0 * NB;
       mi.X = m->vertices;
@@ -386,7 +408,7 @@ __device__ __forceinline__ int t_local_bytes(int n, int lb) { return round_up(n 
 __device__ __forceinline__ int t_xyz_pitch(int vrec) { return round_up(vrec * 8, 16) / 8; }
 __device__ __forceinline__ int t_u_pitch(int vrec) { return round_up(vrec * S, 16) / S; }
 
-template <bool STD>
+template <bool STD, bool GEOM>
 __device__ __forceinline__ void integrate_tiled_body(const TiledLaunchArgs<real>& t) {
   const IntegrateArgs<real>& a = t.a;
   constexpr int SCRATCH_BYTES = Area<false>::BYTES;
@@ -395,10 +417,12 @@ __device__ __forceinline__ void integrate_tiled_body(const TiledLaunchArgs<real>
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int W = a.warps;
   const int o_aux = t_local_bytes(nbc, lb);
-  const int o_rec = o_aux + aux_bytes(nbc);
+  const int o_inv = o_aux + aux_bytes(nbc);
+  const int o_det = o_inv + (GEOM ? inv_bytes(nbc) : 0);
+  const int o_rec = o_det + (GEOM ? det_bytes(nbc) : 0);
   const int o_xyz = o_rec + vrec * 4;
   const int vpitch = t_xyz_pitch(vrec), upitch = t_u_pitch(vrec);
-  const int o_u = o_xyz + D * vpitch * 8;
+  const int o_u = o_xyz + (GEOM ? 0 : D * vpitch * 8);
   const int stage_bytes = o_u + NCOMP * upitch * S;
   unsigned char* scratch_base = smem + a.stages * stage_bytes;
   const PipelineSmem p = carve_pipeline(scratch_base + W * SCRATCH_BYTES);
@@ -422,9 +446,15 @@ __device__ __forceinline__ void integrate_tiled_body(const TiledLaunchArgs<real>
       const uint32_t lbytes = t_local_bytes(nbc, lb), rb = vrec * 4;
       const uint32_t ab = ncell * AUXW * S;
       const bool auxb = AUXW != 0 && t.aux_bulk && (ab & 15u) == 0;
-      mbar_arrive_expect_tx(bar, lbytes + rb + (auxb ? ab : 0));
+      const uint32_t ib = GEOM ? ncell * DD * S : 0, db = GEOM ? ncell * S : 0;
+      const bool geob = GEOM && t.geom_bulk && ((ib | db) & 15u) == 0;
+      mbar_arrive_expect_tx(bar, lbytes + rb + (auxb ? ab : 0) + (geob ? ib + db : 0));
       bulk_g2s(st, t.local + c0 * 4 * lb, lbytes, bar, policy);
       if (auxb) bulk_g2s(st + o_aux, a.aux + c0 * AUXW, ab, bar, policy);
+      if (geob) {
+        bulk_g2s(st + o_inv, a.inv_j + c0 * DD, ib, bar, policy);
+        bulk_g2s(st + o_det, a.det_j + c0, db, bar, policy);
+      }
       bulk_g2s(st + o_rec, t.records + (c0 / nbc) * vrec, rb, bar, policy);
       return true;
     });
@@ -446,8 +476,10 @@ __device__ __forceinline__ void integrate_tiled_body(const TiledLaunchArgs<real>
         real* su = reinterpret_cast<real*>(st + o_u);
         for (int j = lane; j < cnt; j += 32) {
           const int64_t v = rec[4 + j];
+          if constexpr (!GEOM) {
 #pragma unroll
-          for (int i = 0; i < D; ++i) cp_async<8>(sx + i * vpitch + j, t.vertices + v * D + i);
+            for (int i = 0; i < D; ++i) cp_async<8>(sx + i * vpitch + j, t.vertices + v * D + i);
+          }
 #pragma unroll
           for (int c = 0; c < NCOMP; ++c) cp_async<S>(su + c * upitch + j, t.coeffs_global + v * NCOMP + c);
         }
@@ -477,10 +509,17 @@ __device__ __forceinline__ void integrate_tiled_body(const TiledLaunchArgs<real>
     const real* aux_src = (AUXW != 0 && t.aux_bulk && (ab & 15u) == 0) ? reinterpret_cast<const real*>(st + o_aux)
                                                                         : a.aux + c0 * AUXW;
     MeshIn mi{nullptr, nullptr, nullptr, t.bad, c0, st, reinterpret_cast<const double*>(st + o_xyz),
-              reinterpret_cast<const real*>(st + o_u), vpitch, upitch, lb};
+              reinterpret_cast<const real*>(st + o_u), vpitch, upitch, lb, nullptr, nullptr};
+    if constexpr (GEOM) {
+      const uint32_t ib = ncell * DD * S, db = ncell * S;
+      const bool geob = t.geom_bulk && ((ib | db) & 15u) == 0;
+      mi.g_inv = geob ? reinterpret_cast<const real*>(st + o_inv) : a.inv_j + c0 * DD;
+      mi.g_det = geob ? reinterpret_cast<const real*>(st + o_det) : a.det_j + c0;
+    }
     real* out = a.out + c0 * NBC;
     for (int c = warp * CW; c < ncell; c += W * CW)
-      warp_slice<STD, true, SRC_TILED>(a.tab, nullptr, nullptr, nullptr, aux_src, scratch, c, ncell, out, lane, mi);
+      warp_slice<STD, true, GEOM ? SRC_TILED_GEOM : SRC_TILED>(a.tab, nullptr, nullptr, nullptr, aux_src, scratch, c,
+                                                                ncell, out, lane, mi);
     mbar_arrive(&p.empty[stage]);
     if (++stage == a.stages) {
       stage = 0;
@@ -520,11 +559,22 @@ txb_jit_integrate_mesh_std(const __grid_constant__ txb::MeshLaunchArgs<real> m) 
 // tiled mesh entry points (geometry + gather from per-tile vertex tables)
 extern "C" __global__ void __launch_bounds__(txb::MAX_CTA_THREADS, 1)
 txb_jit_integrate_tiled(const __grid_constant__ txb::TiledLaunchArgs<real> t) {
-  txb::jit::integrate_tiled_body<false>(t);
+  txb::jit::integrate_tiled_body<false, false>(t);
 }
 
 extern "C" __global__ void __launch_bounds__(txb::MAX_CTA_THREADS, 1)
 txb_jit_integrate_tiled_std(const __grid_constant__ txb::TiledLaunchArgs<real> t) {
-  txb::jit::integrate_tiled_body<true>(t);
+  txb::jit::integrate_tiled_body<true, false>(t);
+}
+
+// the caller's geometry streamed with the batch, coefficients from the tile tables
+extern "C" __global__ void __launch_bounds__(txb::MAX_CTA_THREADS, 1)
+txb_jit_integrate_tiled_geom(const __grid_constant__ txb::TiledLaunchArgs<real> t) {
+  txb::jit::integrate_tiled_body<false, true>(t);
+}
+
+extern "C" __global__ void __launch_bounds__(txb::MAX_CTA_THREADS, 1)
+txb_jit_integrate_tiled_geom_std(const __grid_constant__ txb::TiledLaunchArgs<real> t) {
+  txb::jit::integrate_tiled_body<true, true>(t);
 }
 #endif

@@ -80,6 +80,7 @@ struct TiledLaunchArgs {
   int vrec;
   int lb;                       // local index bytes, 1 | 2
   int aux_bulk;                 // aux base 16-byte aligned
+  int geom_bulk;                // given geometry (a.inv_j / a.det_j) bases 16-byte aligned
 };
 
 // 16- and 8-byte vector types per element type (type-preserving: the lanes of

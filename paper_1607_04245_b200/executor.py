@@ -346,10 +346,13 @@ def integrate_transposed(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule:
                               cells=cells_dev, vertices=verts_dev, n_bl=n_bl, check_orientation=check)
         if check and cell_geom is None:
             _mark_oriented(cells_dev)
-    elif isinstance(kernel, _backend.JitKernel) and cell_geom is None and os.environ.get("TXB_JIT_MESH", "1") != "0":
-        # run-time compiled form, fused the same way (csrc/txb_jit_kernel.cuh, mesh entry points)
-        elem = _jit_mesh(kernel, mesh, tab, rule, form, glob_dev, aux_dev, dt, cells_dev, verts_dev, n_bl, check)
-        if check:
+    elif (isinstance(kernel, _backend.JitKernel) and os.environ.get("TXB_JIT_MESH", "1") != "0" and
+          (cell_geom is None or _tiled_enabled(mesh, rule))):
+        # run-time compiled form, fused the same way (csrc/txb_jit_kernel.cuh, mesh entry points; given
+        # geometry through the tiled entry point)
+        elem = _jit_mesh(kernel, mesh, tab, rule, form, glob_dev, aux_dev, dt, cells_dev, verts_dev, n_bl,
+                         check and cell_geom is None, cell_geom=cell_geom)
+        if check and cell_geom is None:
             _mark_oriented(cells_dev)
     else:
         if cell_geom is None:
@@ -422,7 +425,7 @@ def _check_aux_shape(aux, n_cells: int, n_b: int, form: PhysicsForm):
 
 
 def _jit_mesh(kernel, mesh: Mesh, tab: Tabulation, rule: QuadratureRule, form: PhysicsForm, glob_dev, aux_dev, dt,
-              cells_dev, verts_dev, n_bl: int, check_orientation: bool = True, out=None):
+              cells_dev, verts_dev, n_bl: int, check_orientation: bool = True, out=None, cell_geom=None):
     """Element vectors of a run-time compiled form straight from the mesh
     (txb_jit_integrate_mesh: float64 geometry + gather in-kernel, any
     tabulation).  Raises OrientationError for a cell with detJ <= 0."""
@@ -440,13 +443,18 @@ def _jit_mesh(kernel, mesh: Mesh, tab: Tabulation, rule: QuadratureRule, form: P
     bad = torch.full((1,), -1, dtype=torch.int64, device="cuda") if check_orientation else None
     B, D, W = (np.ascontiguousarray(x, dtype=dt) for x in (tab.basis, tab.basis_der, rule.weights))
     av = None if aux_dev is None else aux_dev.values.contiguous()
+    inv = det = None
+    if cell_geom is not None:  # (tiled path only: the caller's geometry, cast once to the run precision)
+        inv, det = _dev(cell_geom.inv_jacobians, torch, dt), _dev(cell_geom.determinants, torch, dt)
+        bad = None
     if n > 0 and _tiled_enabled(mesh, rule):
         # per-tile vertex tables (the tiled kernel's design, run-time compiled form)
         tiles = cell_tiles(cells_dev, mesh.dim, default_tile_cells(mesh.dim, rule.n_q))
         rc = _lib.lib().txb_jit_integrate_mesh_tiled(
             ctypes.c_void_p(kernel.handle), n, mesh.n_vertices, B.ctypes.data, D.ctypes.data, W.ctypes.data,
             verts_dev.data_ptr(), tiles.tile_cells, tiles.records.data_ptr(), tiles.vrec, tiles.local.data_ptr(),
-            tiles.local_bytes, glob_dev.data_ptr(), None if av is None else av.data_ptr(), res.data_ptr(),
+            tiles.local_bytes, glob_dev.data_ptr(), None if inv is None else inv.data_ptr(),
+            None if det is None else det.data_ptr(), None if av is None else av.data_ptr(), res.data_ptr(),
             None if bad is None else bad.data_ptr(), _stream_ptr(torch))
         _lib.check(rc, "txb_jit_integrate_mesh_tiled")
     else:

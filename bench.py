@@ -531,6 +531,40 @@ def api_rows(steps=20):
     return rows
 
 
+def residual_graph_rows(steps=50):
+    """The mesh-level residual as a user's solver loop runs it: integrate_transposed
+    (geometry + gather + integration + deterministic scatter-add) captured once as
+    a ResidualGraph, replayed per residual; device time per residual, 2^20-cell
+    3D Kuhn mesh (var-coef P0, f64), global vector device-resident."""
+    import torch
+
+    import paper_1607_04245_b200 as txb
+    from paper_1607_04245_b200.workload import refine_for
+
+    mesh = txb.generate_unit_simplex_mesh(3, refine_for(3, 1 << 20))
+    form = txb.poisson_varcoef_form(3)
+    rule = txb.quadrature_rule(3, 1)
+    tab = txb.tabulate(3, rule)
+    aux = txb.CellAux("p0", torch.rand((mesh.n_cells, 1), dtype=torch.float64, device="cuda") + 0.5)
+    glob = torch.from_numpy(np.random.default_rng(5).standard_normal(mesh.n_vertices)).cuda()
+    rg = txb.ResidualGraph(mesh, txb.FieldLayout(1), tab, rule, form, aux, n_bl=16, n_cb=8, dtype="f64",
+                           shared_mem_limit=None)
+    for _ in range(3):
+        rg(glob)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        rg(glob)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    return [{"config": "residual_graph_3d_varcoef_f64", "cells": mesh.n_cells, "vertices": mesh.n_vertices,
+             "ms_per_residual": ms, "gcells_per_s": mesh.n_cells / (ms * 1e-3) / 1e9,
+             "path": "ResidualGraph: copy-in + one CUDA-graph replay (tiled mesh kernel, in-kernel float64 "
+                     "geometry, + slot-ordered scatter-add); the reference's integrate_transposed ~290 ms"}]
+
+
 def sweep_rows(peak):
     """BASELINE.json configs[4]: 3D P1 var-coef Laplacian at 2^24..2^27 cells on
     one GPU, f32 and f64.  The 2^20-cell Kuhn workload is tiled on the device
@@ -824,16 +858,19 @@ def variant_rows(peak, steps):
 
 
 def variant_steps(n_cells: int, steps: int) -> int:
-    """Launches timed per variant: >= 50 (so a short driver run still averages
-    over many launches), a quarter of K for long runs, capped at 1000."""
-    return min(1000, max(50, steps // 4)) if n_cells <= (1 << 20) else 40
+    """Launches timed per variant: >= 200 (a short driver run still averages
+    over many launches: one graph replay's fixed start costs ~1-2 % of a
+    50-launch chain of 10 us launches), a quarter of K for long runs, capped at
+    1000."""
+    return min(1000, max(200, steps // 4)) if n_cells <= (1 << 20) else 40
 
 
-def mesh_rows(peak, steps):
+def mesh_rows(peak, steps, configs=("3d_varcoef_f64", "3d_varcoef_f32", "3d_elasticity_f64", "3d_elasticity_f32",
+                                     "2d_varcoef_f64", "2d_varcoef_f32"),
+              modes=("given", "given_tiled", "tiled", "per_cell")):
     rows = []
-    for v in ("3d_varcoef_f64", "3d_varcoef_f32", "3d_elasticity_f64", "3d_elasticity_f32", "2d_varcoef_f64",
-              "2d_varcoef_f32"):
-        for mode in ("given", "given_tiled", "tiled", "per_cell"):
+    for v in configs:
+        for mode in modes:
             def one(v=v, mode=mode):
                 vf, _ = config_model(v)
                 n = CONFIGS[v][3]
@@ -1019,6 +1056,10 @@ def main():
             peak = line["roofline"]["peak"]
             if not args.no_variants:
                 rows += variant_rows(peak, args.steps)
+                # the mesh-level path (§8f rows 1 + 3): the tiled kernel, geometry in-kernel and given
+                rows += mesh_rows(peak, args.steps, configs=("3d_varcoef_f64", "3d_varcoef_f32"),
+                                  modes=("tiled", "given_tiled"))
+                _guarded(rows, "residual_graph", residual_graph_rows)
             if args.extras:
                 rows += mesh_rows(peak, args.steps)
                 _guarded(rows, "sweep", sweep_rows, peak)

@@ -412,7 +412,9 @@ static int compute_geometry(const Config& c, const KernelInfo& k, int64_t n_cell
     // (whole rounds of the resident grid) are dealt round-robin first.
     const int64_t n_batches = (n_cells + g.n_bc - 1) / g.n_bc;
     const int64_t r = std::max<int64_t>(1, std::min<int64_t>(n_batches, resident));
-    const int pct = std::min(100, std::max(0, env_int("TXB_STATIC_PCT", 60)));
+    // share of the batches dealt round-robin first (2D elasticity f32: 40 %, profiles/r2as_pct.md)
+    const int pct_default = (c.dim == 2 && c.n_comp == 2 && c.dtype == 4 && k.family == FAMILY_CELLS) ? 40 : 60;
+    const int pct = std::min(100, std::max(0, env_int("TXB_STATIC_PCT", pct_default)));
     g.static_batches = n_batches * pct / 100 / r * r;
     g.resident = g.static_batches > 0 ? (int)r : 0;
     const int64_t units = g.resident + (n_batches - g.static_batches);

@@ -650,23 +650,27 @@ class _null:
         return False
 
 
-def time_e2e(wl, steps, warmup):
-    """Through the reference-facing call with HOST buffers (pinned numpy):
-    H2D + kernel + D2H per step inside the timed region (wall clock; the host
-    call returns only after the result is in host memory)."""
+def time_e2e(wl, steps, warmup, pageable=False):
+    """Through the reference-facing call with HOST buffers (pinned numpy; or
+    plain pageable numpy arrays with ``pageable``): H2D + kernel + D2H per step
+    inside the timed region (wall clock; the host call returns only after the
+    result is in host memory)."""
     import torch
 
     from paper_1607_04245_b200 import backend
     from paper_1607_04245_b200.physics import CellAux
 
     def pinned(t):
+        if pageable:
+            return t.cpu().numpy().copy()
         h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
         h.copy_(t)
         return h.numpy()
 
     inv, det, co = pinned(wl["inv"]), pinned(wl["det"]), pinned(wl["coeffs"])
     aux = None if wl["aux"] is None else CellAux("p0", pinned(wl["aux"].values))
-    out = torch.empty(tuple(co.shape), dtype=wl["coeffs"].dtype, pin_memory=True).numpy()
+    out = (np.empty(tuple(co.shape), dtype=co.dtype) if pageable else
+           torch.empty(tuple(co.shape), dtype=wl["coeffs"].dtype, pin_memory=True).numpy())
     tab, rule = wl["tab"], wl["rule"]
     kernel = backend.cuda_kernel(wl["form"], rule.n_q, wl["aux"], co.dtype.itemsize)
     npdt = co.dtype
@@ -1048,6 +1052,12 @@ def main():
                                     "frac_of_h2d_floor": floor_ms / (e2e_s / e2e_steps * 1e3)})
             except Exception as e:  # noqa: BLE001
                 line["e2e"]["h2d_link_error"] = f"{type(e).__name__}: {e}"
+            # the same call with plain pageable numpy arrays (a reference user's buffers): context
+            try:
+                ps, _, _, _ = time_e2e(wl, 5, 1, pageable=True)
+                line["e2e"]["pageable_value"] = flops_cell * wl["n"] * 5 / ps / 1e9
+            except Exception as e:  # noqa: BLE001
+                line["e2e"]["pageable_error"] = f"{type(e).__name__}: {e}"
     try:
         # -------------------------------------------------------------- extras
         # (each row group guarded: a failure is an error row, never a lost headline)

@@ -77,7 +77,7 @@ __device__ __forceinline__ void warp_slice(const Tabulation<T>& tab, const T* __
       T J[DD];
       load_row<T, DD, VEC>(s_inv + cell * DD, J);
       T cf[NBC];
-      load_row<T, NBC, VEC>(s_coef + cell * NBC, cf);
+      load_row_rot<T, NBC, VEC>(s_coef + cell * NBC, cf, lane);
       const T det = s_det[cell];
 
       T tr[NB][D];
@@ -136,7 +136,7 @@ __device__ __forceinline__ void warp_slice(const Tabulation<T>& tab, const T* __
         a0 = s_aux[cell];
       } else if constexpr (AUX == 2) {
         T av[NB];
-        load_row<T, NB, VEC>(s_aux + cell * AUXW, av);
+        load_row_rot<T, NB, VEC>(s_aux + cell * AUXW, av, lane);
         const T* Bq = tab.B + q * NB;
         a0 = mul(av[0], Bq[0]);
 #pragma unroll

@@ -167,7 +167,7 @@ __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const re
       det = (real)detd;
     } else {
       load_row<real, DD, VEC>(s_inv + cell * DD, J);
-      load_row<real, NBC, VEC>(s_coef + cell * NBC, cf);
+      load_row_rot<real, NBC, VEC>(s_coef + cell * NBC, cf, lane);
       det = s_det[cell];
     }
 

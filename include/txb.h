@@ -188,6 +188,13 @@ int txb_integrate_mesh_tiled(int form_code, int aux_mode, int dtype_bytes, int d
 int txb_debug_geometry_fast(int dim, int64_t n_cells, const double* vertices, const int64_t* cells,
                             double* inv_j, double* det_j, int32_t* ok, int exact_zero, void* stream);
 
+/* Test hook: the float32 runs' branch-free geometry (float32 of the float64
+ * quotient from one product by RN(1/det); ok[c] = 0 where a quotient is near a
+ * float32 rounding midpoint or out of range and the kernels recompute it).
+ * inv_j / det_j float32.  Device pointers, asynchronous. */
+int txb_debug_geometry_fast32(int dim, int64_t n_cells, const double* vertices, const int64_t* cells,
+                              float* inv_j, float* det_j, int32_t* ok, void* stream);
+
 /* Gather per-cell coefficient blocks (device pointers):
  *   out[c][b][k] = global[cells[c][b] * n_comp + k],  cells int64 (n, n_b). */
 int txb_gather_coefficients(int dtype_bytes, int64_t n_cells, int n_b, int n_comp,

@@ -38,6 +38,7 @@ SIGNATURES = {
     "txb_integrate_mesh_tiled": (_I, [_I, _I, _I, _I, _I, _I, c_int64, c_int64, _P, _P, _P, _P, _I, _P, _I, _P,
                                       _I, _P, _P, _P, _P, _P, _P, _P]),
     "txb_debug_geometry_fast": (_I, [_I, c_int64, _P, _P, _P, _P, _P, _I, _P]),
+    "txb_debug_geometry_fast32": (_I, [_I, c_int64, _P, _P, _P, _P, _P, _P]),
     "txb_gather_coefficients": (_I, [_I, c_int64, _I, _I, _P, _P, _P, _P]),
     "txb_scatter_add": (_I, [_I, c_int64, _I, _P, _P, _P, _P, _P]),
     "txb_scatter_add_slots": (_I, [_I, c_int64, _I, _P, _P, _P, _P, _P, _P]),

@@ -251,18 +251,15 @@ __device__ __forceinline__ bool dd_range_bad(double x) {
   return (hi - 0x20B00000u > 0x3E800000u) & ((hi | lo) != 0u);
 }
 
-// EXACT_ZERO: a zero numerator returns itself (+-0, = numpy's x / det for
-// det > 0) instead of +0 -- for callers that can see the sign of a zero
-// geometry entry (the run-time compiled user forms); then every accepted cell
-// is bit-identical to affine_inverse.
-template <int D, bool EXACT_ZERO = false>
-__device__ __forceinline__ bool affine_inverse_fast(const double (&X)[D + 1][D], double (&inv)[D * D], double& det) {
+// The reference's cofactor numerators (numpy's expression order, as
+// affine_inverse) and det.
+template <int D>
+__device__ __forceinline__ void affine_numerators(const double (&X)[D + 1][D], double (&num)[D * D], double& det) {
   double m[D][D];
 #pragma unroll
   for (int k = 0; k < D; ++k)
 #pragma unroll
     for (int i = 0; i < D; ++i) m[i][k] = __dsub_rn(X[k + 1][i], X[0][i]);
-  double num[D * D];
   if constexpr (D == 2) {
     const double a = m[0][0], b = m[0][1], c = m[1][0], e = m[1][1];
     det = __dsub_rn(__dmul_rn(a, e), __dmul_rn(b, c));
@@ -282,6 +279,16 @@ __device__ __forceinline__ bool affine_inverse_fast(const double (&X)[D + 1][D],
     num[5] = __dsub_rn(__dmul_rn(m[0][2], m[1][0]), __dmul_rn(m[0][0], m[1][2]));
     num[8] = __dsub_rn(__dmul_rn(m[0][0], m[1][1]), __dmul_rn(m[0][1], m[1][0]));
   }
+}
+
+// EXACT_ZERO: a zero numerator returns itself (+-0, = numpy's x / det for
+// det > 0) instead of +0 -- for callers that can see the sign of a zero
+// geometry entry (the run-time compiled user forms); then every accepted cell
+// is bit-identical to affine_inverse.
+template <int D, bool EXACT_ZERO = false>
+__device__ __forceinline__ bool affine_inverse_fast(const double (&X)[D + 1][D], double (&inv)[D * D], double& det) {
+  double num[D * D];
+  affine_numerators<D>(X, num, det);
   // det > 0 in range: the signed high word within [2^-500, 2^500]
   bool bad = ((unsigned)__double2hiint(det) - 0x20B00000u) > 0x3E800000u;
 #if TXB_DD_RECIPROCAL
@@ -312,6 +319,63 @@ __device__ __forceinline__ bool affine_inverse_fast(const double (&X)[D + 1][D],
   }
 #endif
   return !bad;
+}
+
+// float32 runs (the reference computes float64 geometry and casts it,
+// executor._device_arrays): only float32(RN64(x / det)) is needed.  With
+// y = RN(1/det) and q = RN(x y), |q - x/det| <= 2 ulp and so |q - RN64(x/det)|
+// <= 3 ulp (bit-pattern distance, det and x/det in range).  float32 rounding of
+// a double only changes across a float32 rounding midpoint (low 29 mantissa
+// bits 0x10000000); when no midpoint lies within 8 ulp of q, float32(q) =
+// float32(RN64(x/det)).  One product per quotient instead of the four of the
+// correctly rounded double path.  The cell is rejected (the caller redoes it
+// exactly) if det leaves [2^-500, 2^500], a nonzero quotient leaves the
+// float32-normal range [2^-125, 2^127) or lies near a midpoint (~3e-7 of
+// cells).  A zero numerator gives x * y = x: the sign of a zero is kept.
+template <int D>
+__device__ __forceinline__ bool affine_inverse_fast32(const double (&X)[D + 1][D], float (&inv)[D * D], double& det) {
+  double num[D * D];
+  affine_numerators<D>(X, num, det);
+  bool bad = ((unsigned)__double2hiint(det) - 0x20B00000u) > 0x3E800000u;
+  const double y = __drcp_rn(det);
+#pragma unroll
+  for (int i = 0; i < D * D; ++i) {
+    const double x = num[i];
+    const double q = __dmul_rn(x, y);
+    const unsigned hi = (unsigned)__double2hiint(q) & 0x7fffffffu, lo = (unsigned)__double2loint(q);
+    const bool near_mid = ((lo & 0x1FFFFFFFu) - 0x0FFFFFF8u) < 17u;
+    const bool out_of_range = (hi - 0x38200000u) >= (0x47E00000u - 0x38200000u);
+    bad |= (x != 0.0) & (near_mid | out_of_range);
+    inv[i] = __double2float_rn(q);
+  }
+  return !bad;
+}
+
+// One cell's geometry in the run precision: the float64 quotients cast once
+// (executor._device_arrays, executor.py:77-90) -- the branch-free paths above,
+// affine_inverse for a rejected cell.  detd (float64) is for the orientation
+// check.
+template <typename T, int D, bool EXACT_ZERO = false>
+__device__ __forceinline__ void cell_geometry(const double (&X)[D + 1][D], T (&J)[D * D], T& det, double& detd) {
+  bool ok;
+  if constexpr (sizeof(T) == 4) {
+    float inv[D * D];
+    ok = affine_inverse_fast32<D>(X, inv, detd);
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) J[i] = (T)inv[i];
+  } else {
+    double inv[D * D];
+    ok = affine_inverse_fast<D, EXACT_ZERO>(X, inv, detd);
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) J[i] = (T)inv[i];
+  }
+  if (!ok) {
+    double inv[D * D];
+    affine_inverse<D>(X, inv, detd);
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) J[i] = (T)inv[i];
+  }
+  det = (T)detd;
 }
 
 __host__ __device__ constexpr int round_up(int x, int m) { return (x + m - 1) / m * m; }

@@ -126,13 +126,9 @@ __device__ __forceinline__ void mesh_slice(const MeshArgs<T>& a, const int64_t* 
         for (int b = 0; b < NB; ++b)
 #pragma unroll
           for (int i = 0; i < D; ++i) X[b][i] = __ldg(a.vertices + ids[b] * D + i);
-        double inv[DD], detd;
-        if (!affine_inverse_fast<D>(X, inv, detd)) affine_inverse<D>(X, inv, detd);  // branch-free; exact fallback
+        double detd;
+        cell_geometry<T, D>(X, J, det, detd);  // branch-free; exact fallback
         if (q == 0 && a.bad && detd <= 0.0) atomicMin(a.bad, (unsigned long long)(c0_batch + cell));
-        // executor._device_arrays (executor.py:77-90): cast once to the run precision
-#pragma unroll
-        for (int i = 0; i < DD; ++i) J[i] = (T)inv[i];
-        det = (T)detd;
       } else {
         load_row<T, DD, SMEM>(s_inv + cell * DD, J);
         det = s_det[cell];

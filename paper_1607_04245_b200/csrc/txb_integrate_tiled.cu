@@ -292,12 +292,9 @@ __device__ __forceinline__ void tiled_slice(const TiledArgs<T>& a, const unsigne
       for (int b = 0; b < NB; ++b)
 #pragma unroll
         for (int i = 0; i < D; ++i) X[b][i] = sx[i * vpitch + ids[b]];
-      double inv[DD], detd;
-      if (!affine_inverse_fast<D>(X, inv, detd)) affine_inverse<D>(X, inv, detd);  // rare: out-of-range scales
+      double detd;
+      cell_geometry<T, D>(X, J, det, detd);
       if (q == 0 && a.bad && detd <= 0.0) atomicMin(a.bad, (unsigned long long)(c0_batch + cell));
-#pragma unroll
-      for (int i = 0; i < DD; ++i) J[i] = (T)inv[i];  // executor._device_arrays: cast once
-      det = (T)detd;
     }
 
     // standard P1 pull-back (exactness note in txb_kernels.cuh)
@@ -692,9 +689,44 @@ __global__ void geometry_fast_kernel(const double* __restrict__ vertices, const 
   det_out[c] = det;
 }
 
+template <int D>
+__global__ void geometry_fast32_kernel(const double* __restrict__ vertices, const int64_t* __restrict__ cells,
+                                       int64_t n, float* __restrict__ inv_out, float* __restrict__ det_out,
+                                       int32_t* __restrict__ ok_out) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  double X[D + 1][D];
+#pragma unroll
+  for (int b = 0; b <= D; ++b)
+#pragma unroll
+    for (int i = 0; i < D; ++i) X[b][i] = vertices[cells[c * (D + 1) + b] * D + i];
+  float inv[D * D];
+  double det;
+  ok_out[c] = affine_inverse_fast32<D>(X, inv, det) ? 1 : 0;
+#pragma unroll
+  for (int i = 0; i < D * D; ++i) inv_out[c * D * D + i] = inv[i];
+  det_out[c] = (float)det;
+}
+
 }  // namespace txb
 
 using namespace txb;
+
+extern "C" int txb_debug_geometry_fast32(int dim, int64_t n_cells, const double* vertices, const int64_t* cells,
+                                         float* inv_j, float* det_j, int32_t* ok, void* stream) {
+  if (n_cells <= 0) return TXB_OK;
+  const unsigned blocks = (unsigned)((n_cells + 255) / 256);
+  if (dim == 2)
+    geometry_fast32_kernel<2><<<blocks, 256, 0, (cudaStream_t)stream>>>(vertices, cells, n_cells, inv_j, det_j, ok);
+  else if (dim == 3)
+    geometry_fast32_kernel<3><<<blocks, 256, 0, (cudaStream_t)stream>>>(vertices, cells, n_cells, inv_j, det_j, ok);
+  else {
+    set_error("dim must be 2 or 3");
+    return TXB_E_UNSUPPORTED;
+  }
+  TXB_CUDA_TRY(cudaGetLastError());
+  return TXB_OK;
+}
 
 extern "C" int txb_debug_geometry_fast(int dim, int64_t n_cells, const double* vertices, const int64_t* cells,
                                        double* inv_j, double* det_j, int32_t* ok, int exact_zero, void* stream) {

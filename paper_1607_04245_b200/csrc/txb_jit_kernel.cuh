@@ -157,14 +157,11 @@ __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const re
 #pragma unroll
           for (int i = 0; i < D; ++i) X[b][i] = __ldg(mi.X + ids[b] * D + i);
       }
-      double inv[DD], detd;
-      // branch-free correctly rounded quotients, signed zeros kept (user forms may see them);
-      // exact division for the rare out-of-range cell
-      if (!affine_inverse_fast<D, true>(X, inv, detd)) affine_inverse<D>(X, inv, detd);
+      double detd;
+      // branch-free quotients, signed zeros kept (user forms may see them);
+      // exact division for the rare rejected cell
+      cell_geometry<real, D, true>(X, J, det, detd);
       if (q == 0 && mi.bad && detd <= 0.0) atomicMin(mi.bad, (unsigned long long)(mi.c0_batch + cell));
-#pragma unroll
-      for (int i = 0; i < DD; ++i) J[i] = (real)inv[i];
-      det = (real)detd;
     } else {
       load_row<real, DD, VEC>(s_inv + cell * DD, J);
       load_row_rot<real, NBC, VEC>(s_coef + cell * NBC, cf, lane);

@@ -245,6 +245,116 @@ def test_branch_free_geometry_is_correctly_rounded(dim, seed, exact_zero):
         assert np.array_equal(a.view(np.int64), b.view(np.int64))
 
 
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("seed", [0, 1])
+def test_branch_free_float32_geometry(dim, seed):
+    """affine_inverse_fast32 (float32 runs: one product by RN(1/det) per
+    quotient, a midpoint-distance test instead of the correction) against
+    float32(numpy's correctly rounded float64 x / det) on 2^20 random simplices:
+    every accepted cell is bit-identical, signed zeros included; cells whose
+    quotient is out of the float32-normal range are rejected."""
+    from paper_1607_04245_b200 import _lib
+
+    rng = np.random.default_rng(200 + seed)
+    n = 1 << 20
+    scale = 10.0 ** rng.uniform(-6, 6, (n, 1, 1))
+    x = rng.uniform(-1, 1, (n, dim + 1, dim)) * scale
+    x[: n // 8] = np.round(x[: n // 8] * 64) / 64
+    x[n // 8: n // 4] *= 2.0 ** rng.integers(-300, 300, (n // 8, 1, 1))
+    verts = x.reshape(-1, dim)
+    cells = np.arange(n * (dim + 1), dtype=np.int64).reshape(n, dim + 1)
+    with np.errstate(all="ignore"):
+        _, det = oracle.geometry(verts, cells)
+        flip = det < 0
+        cells[flip, 1], cells[flip, 2] = cells[flip, 2].copy(), cells[flip, 1].copy()
+        inv, det = oracle.geometry(verts, cells)
+        inv32, det32 = inv.astype(np.float32), det.astype(np.float32)
+    V = torch.from_numpy(verts).cuda()
+    C = torch.from_numpy(cells).cuda()
+    inv_d = torch.empty((n, dim, dim), dtype=torch.float32, device="cuda")
+    det_d = torch.empty(n, dtype=torch.float32, device="cuda")
+    ok = torch.empty(n, dtype=torch.int32, device="cuda")
+    _lib.check(_lib.lib().txb_debug_geometry_fast32(dim, n, V.data_ptr(), C.data_ptr(), inv_d.data_ptr(),
+                                                    det_d.data_ptr(), ok.data_ptr(), None))
+    torch.cuda.synchronize()
+    okh = ok.cpu().numpy().astype(bool)
+    assert bitwise_equal(det_d.cpu().numpy(), det32)
+    assert okh[: n // 8][det[: n // 8] > 0].all() and okh.mean() > 0.8
+    assert ((det > 0) | ~okh).all()
+    a, b = inv_d.cpu().numpy()[okh], inv32[okh]
+    assert np.array_equal(a.view(np.int32), b.view(np.int32))
+    with np.errstate(all="ignore"):
+        big = (np.abs(inv) >= 2.0 ** 127).any(axis=(1, 2)) | ((np.abs(inv) < 2.0 ** -125) & (inv != 0)).any(axis=(1, 2))
+    assert not okh[big].any()
+
+
+def test_float32_geometry_rejects_quotients_near_a_rounding_midpoint():
+    """A quotient within a few double ulps of a float32 rounding midpoint
+    (here 1/e with e = RN(1/(1 + 2^-24)), ~1 + 2^-24) is not decided by the
+    one-product shortcut: the cell is rejected and the kernels redo it
+    exactly; a neighbouring well-separated cell is accepted."""
+    from paper_1607_04245_b200 import _lib
+
+    e = 1.0 / (1.0 + 2.0 ** -24)
+    verts = np.array([[0, 0], [1, 0], [0, e], [0, 0], [1, 0], [0, 0.75]], dtype=np.float64)
+    cells = np.array([[0, 1, 2], [3, 4, 5]], dtype=np.int64)
+    inv, det = oracle.geometry(verts, cells)
+    V = torch.from_numpy(verts).cuda()
+    C = torch.from_numpy(cells).cuda()
+    inv_d = torch.empty((2, 2, 2), dtype=torch.float32, device="cuda")
+    det_d = torch.empty(2, dtype=torch.float32, device="cuda")
+    ok = torch.empty(2, dtype=torch.int32, device="cuda")
+    _lib.check(_lib.lib().txb_debug_geometry_fast32(2, 2, V.data_ptr(), C.data_ptr(), inv_d.data_ptr(),
+                                                    det_d.data_ptr(), ok.data_ptr(), None))
+    torch.cuda.synchronize()
+    assert ok.cpu().tolist() == [0, 1]
+    assert bitwise_equal(inv_d.cpu().numpy()[1], inv[1].astype(np.float32))
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_float32_mesh_near_midpoint_cells_bitwise(dim, monkeypatch):
+    """The fused kernels redo a rejected cell exactly: on a structured mesh
+    stretched by e = RN(1/(1 + 2^-24)) along one axis, invJ entries sit on
+    float32 rounding midpoints (the shortcut rejects those cells), and the
+    float32 mesh integration is still bit-identical to the oracle (float64
+    geometry cast once) on every path that computes geometry in-kernel."""
+    from paper_1607_04245_b200 import _lib
+
+    n = 8 if dim == 2 else 4
+    base = txb.generate_unit_simplex_mesh(dim, n)
+    v = np.array(base.vertices, dtype=np.float64)
+    v[:, 1] *= 1.0 / (1.0 + 2.0 ** -24)
+    mesh = txb.Mesh(dim, v, base.cells)
+    V = torch.from_numpy(v).cuda()
+    C = torch.from_numpy(np.ascontiguousarray(mesh.cells)).cuda()
+    nc = mesh.n_cells
+    inv_d = torch.empty((nc, dim, dim), dtype=torch.float32, device="cuda")
+    det_d = torch.empty(nc, dtype=torch.float32, device="cuda")
+    ok = torch.empty(nc, dtype=torch.int32, device="cuda")
+    _lib.check(_lib.lib().txb_debug_geometry_fast32(dim, nc, V.data_ptr(), C.data_ptr(), inv_d.data_ptr(),
+                                                    det_d.data_ptr(), ok.data_ptr(), None))
+    torch.cuda.synchronize()
+    assert (ok.cpu().numpy() == 0).any()  # the fallback is exercised
+    rng = np.random.default_rng(dim)
+    for factory, aux_space in FORMS:
+        form = factory(dim)
+        glob = rng.standard_normal(mesh.n_vertices * form.n_comp)
+        aux = None
+        if aux_space == "p0":
+            aux = txb.CellAux("p0", rng.uniform(0.5, 1.5, (nc, 1)))
+        elif aux_space == "p1":
+            aux = txb.CellAux("p1", rng.uniform(0.5, 1.5, (mesh.n_vertices, 1))[mesh.cells])
+        layout = txb.FieldLayout(form.n_comp)
+        rule = txb.quadrature_rule(dim, 1)
+        tab = txb.tabulate(dim, rule)
+        ref = _oracle(mesh, form, glob, aux, rule, np.float32)
+        g = torch.from_numpy(glob.astype(np.float32)).cuda()
+        for tiled in ("1", "0"):
+            monkeypatch.setenv("TXB_TILED", tiled)
+            out = txb.integrate_mesh(mesh, layout, tab, rule, form, g, aux, dtype="f32").cpu().numpy()
+            assert bitwise_equal(out, ref), (form.name, aux_space, tiled)
+
+
 def test_tile_builder_rejects_out_of_range_ids():
     cells = torch.tensor([[0, 1, 2, 3], [1, 2, 3, (1 << 31) + 5]], dtype=torch.int64, device="cuda")
     with pytest.raises(IndexError):

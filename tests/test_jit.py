@@ -258,22 +258,31 @@ def test_jit_standard_table_entry_point_matches_generic(name, dim, monkeypatch):
 @pytest.mark.parametrize("dim", [2, 3])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 @pytest.mark.parametrize("tiled", ["1", "0"])
-def test_integrate_transposed_user_forms_mesh_fused(name, dim, dtype, tiled, monkeypatch):
+@pytest.mark.parametrize("stretch", [False, True])
+def test_integrate_transposed_user_forms_mesh_fused(name, dim, dtype, tiled, stretch, monkeypatch):
     """integrate_transposed with a run-time compiled form: the mesh entry point
     (float64 geometry + gather in-kernel, txb_jit_integrate_mesh) on a perturbed
     Kuhn mesh with a shuffled vertex numbering, midpoint and two-point rules,
     then the scatter-add — bit-identical to the oracle's geometry -> gather ->
     python-lane integration -> np.add.at, and to the unfused route (given
     geometry: gather + txb_jit_integrate).  tiled = 1: the tiled mesh entry
-    point (txb_jit_integrate_mesh_tiled, per-tile vertex tables)."""
+    point (txb_jit_integrate_mesh_tiled, per-tile vertex tables).  stretch:
+    an unperturbed mesh stretched by RN(1/(1 + 2^-24)) along y, whose invJ
+    entries sit on float32 rounding midpoints (the float32 geometry shortcut
+    rejects those cells and the kernels redo them exactly)."""
+    if stretch and dtype == "f64":
+        pytest.skip("midpoint cells only matter for the float32 geometry path")
     monkeypatch.setenv("TXB_TILED", tiled)
     s = user_forms.spec(name, dim)
     f = form_of(name, dim)
     npdt = np.float64 if dtype == "f64" else np.float32
-    base = txb.generate_unit_simplex_mesh(dim, 11 if dim == 2 else 4)
+    base = txb.generate_unit_simplex_mesh(dim, (8 if stretch else 11) if dim == 2 else 4)
     rng = np.random.default_rng(dim * 7 + len(name))
     perm = rng.permutation(base.n_vertices)
-    verts = base.vertices[np.argsort(perm)] + 0.02 * rng.uniform(-1, 1, base.vertices.shape)
+    if stretch:
+        verts = base.vertices[np.argsort(perm)] * np.array([1.0, 1.0 / (1.0 + 2.0 ** -24), 1.0][:dim])
+    else:
+        verts = base.vertices[np.argsort(perm)] + 0.02 * rng.uniform(-1, 1, base.vertices.shape)
     mesh = txb.Mesh(dim, np.ascontiguousarray(verts), np.ascontiguousarray(perm[base.cells]))
     layout = txb.FieldLayout(s["n_comp"])
     glob = rng.standard_normal(layout.global_size(mesh))

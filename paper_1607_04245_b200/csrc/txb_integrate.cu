@@ -213,8 +213,29 @@ __device__ __forceinline__ void warp_slice(const Tabulation<T>& tab, const T* __
   __syncwarp();  // scratch is reused by the next slice
 }
 
+// Register budget per instantiation.  The elasticity kernels need ~130-190
+// registers without spills (3D, standard tables); under the 544-thread bound
+// ptxas held them to 96 with spills.  A 256-thread CTA bound (<= 7 consumer
+// warps, 128 registers, 2 CTAs/SM guaranteed) is faster for every elasticity
+// configuration but 2D f32, whose small rows favour wide CTAs
+// (profiles/r2bd_bounds.md: 3D f32 24.2 -> 22.7 us, 3D f64 45.5 -> 43.3,
+// 2D f64 23.0 -> 22.4; 2D f32 11.9 -> 13.5 with it).  TXB_ELAST_THREADS /
+// TXB_ELAST_MINB override it in tuning builds.
+template <typename T, int D, int NCOMP>
+struct CtaBound {
+#ifdef TXB_ELAST_THREADS
+  static constexpr bool NARROW = NCOMP > 1;
+  static constexpr int THREADS = NARROW ? TXB_ELAST_THREADS : MAX_CTA_THREADS;
+  static constexpr int MIN_BLOCKS = NARROW ? TXB_ELAST_MINB : 1;
+#else
+  static constexpr bool NARROW = NCOMP > 1 && !(D == 2 && sizeof(T) == 4);
+  static constexpr int THREADS = NARROW ? 256 : MAX_CTA_THREADS;
+  static constexpr int MIN_BLOCKS = NARROW ? 2 : 1;
+#endif
+};
+
 template <typename T, int D, int NQ, int NCOMP, int FORM, int AUX, bool STD>
-__global__ void __launch_bounds__(MAX_CTA_THREADS, 1)
+__global__ void __launch_bounds__(CtaBound<T, D, NCOMP>::THREADS, CtaBound<T, D, NCOMP>::MIN_BLOCKS)
 integrate_kernel(const __grid_constant__ IntegrateArgs<T> a) {
   constexpr int DD = D * D, NBC = (D + 1) * NCOMP;
   using L = StageLayout<T, D, NCOMP, AUX>;
@@ -331,6 +352,7 @@ static bool pick_form(const Config& c, KernelInfo& k) {
   } else if (c.form == 2) {
     using K = Kernel<T, D, NQ, D, 2, 0, STD>;
     k = {K::fn(), K::stage_bytes, K::scratch, K::CW};
+    k.max_warps = CtaBound<T, D, D>::THREADS / 32 - 1;
   } else {
     return false;
   }

@@ -600,15 +600,16 @@ def sweep_rows(peak):
 
 
 def jit_rows(peak, steps):
-    """Run-time compiled lane: the shipped var-coef form through NVRTC (same
-    bytes as the headline) and a user form with f0 + 2 P1 fields + grad a."""
+    """Run-time compiled lane: the shipped var-coef and elasticity forms through
+    NVRTC (same bytes as the ahead-of-time rows) and a user form with f0 + 2 P1
+    fields + grad a."""
     import torch
 
     from paper_1607_04245_b200.perf_model import compulsory_bytes_per_cell
     from paper_1607_04245_b200.physics import CellAux, user_form
 
     rows = []
-    for name in ("3d_varcoef_f64", "3d_varcoef_f32"):
+    for name in ("3d_varcoef_f64", "3d_varcoef_f32", "3d_elasticity_f64", "3d_elasticity_f32"):
         vf, vb = config_model(name)
         wl = rank_workload(name, 0, 1)
         ns = max(4, -(-3 * L2_BYTES // (vb * wl["n"])) + 1)

@@ -528,13 +528,25 @@ __device__ __forceinline__ void integrate_tiled_body(const TiledLaunchArgs<real>
 }  // namespace jit
 }  // namespace txb
 
+// CTA bound of the cell-array and per-cell mesh entry points (the host's
+// jit_cta_threads): multi-component float64 forms get 256 threads and 2 CTAs
+// per SM (128 registers, as the ahead-of-time kernels' CtaBound), the rest the
+// wide bound -- measured on the shipped 3D elasticity form through NVRTC:
+// f64 44.7 -> 43.9 us, while f32 went 24.8 -> 27.8 us with the narrow bound.
+#ifdef TXB_JIT_WIDE  // TXB_JIT_WIDE=1 in the environment: the wide bound for every form (tuning)
+#define TXB_JIT_NARROW 0
+#else
+#define TXB_JIT_NARROW (TXB_NCOMP > 1 && sizeof(real) == 8)
+#endif
+#define TXB_JIT_BOUNDS __launch_bounds__(TXB_JIT_NARROW ? 256 : txb::MAX_CTA_THREADS, TXB_JIT_NARROW ? 2 : 1)
+
 #ifndef TXB_JIT_MESH
-extern "C" __global__ void __launch_bounds__(txb::MAX_CTA_THREADS, 1)
+extern "C" __global__ void TXB_JIT_BOUNDS
 txb_jit_integrate(const __grid_constant__ txb::IntegrateArgs<real> a) {
   txb::jit::integrate_body<false, false>(a, nullptr);
 }
 
-extern "C" __global__ void __launch_bounds__(txb::MAX_CTA_THREADS, 1)
+extern "C" __global__ void TXB_JIT_BOUNDS
 txb_jit_integrate_std(const __grid_constant__ txb::IntegrateArgs<real> a) {
   txb::jit::integrate_body<true, false>(a, nullptr);
 }
@@ -543,12 +555,12 @@ txb_jit_integrate_std(const __grid_constant__ txb::IntegrateArgs<real> a) {
 // mesh-fused: connectivity in, geometry + gather in-kernel (the reference's
 // compute_geometry -> gather_coefficients -> cast -> integrate, executor.py:194-212).
 // A second program (TXB_JIT_MESH), compiled on first use by txb_jit_integrate_mesh.
-extern "C" __global__ void __launch_bounds__(txb::MAX_CTA_THREADS, 1)
+extern "C" __global__ void TXB_JIT_BOUNDS
 txb_jit_integrate_mesh(const __grid_constant__ txb::MeshLaunchArgs<real> m) {
   txb::jit::integrate_body<false, true>(m.a, &m);
 }
 
-extern "C" __global__ void __launch_bounds__(txb::MAX_CTA_THREADS, 1)
+extern "C" __global__ void TXB_JIT_BOUNDS
 txb_jit_integrate_mesh_std(const __grid_constant__ txb::MeshLaunchArgs<real> m) {
   txb::jit::integrate_body<true, true>(m.a, &m);
 }

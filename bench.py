@@ -313,7 +313,7 @@ def time_mesh(name, steps, warmup, n_sets_min=4, given_geometry=False, tiled=Tru
     rule = txb.quadrature_rule(dim, 1)
     tab = txb.tabulate(dim, rule)
     s = np.dtype(npdt).itemsize
-    per_cell = (dim + 1) * 8 + (s if aux_space == "p0" else 0) + (dim + 1) * form.n_comp * s
+    per_cell = (dim + 1) * 8 + {"p0": s, "p1": (dim + 1) * s}.get(aux_space, 0) + (dim + 1) * form.n_comp * s
     cells0 = torch.from_numpy(mesh.cells).cuda()
     os.environ["TXB_TILED"] = "1" if tiled else "0"
     tiles = None
@@ -335,6 +335,8 @@ def time_mesh(name, steps, warmup, n_sets_min=4, given_geometry=False, tiled=Tru
         aux = None
         if aux_space == "p0":
             aux = txb.CellAux("p0", torch.rand((n, 1), dtype=glob.dtype, device="cuda") + 0.5)
+        elif aux_space == "p1":
+            aux = txb.CellAux("p1", torch.rand((n, dim + 1, 1), dtype=glob.dtype, device="cuda") + 0.5)
         sets.append((cells0.clone(), aux, torch.empty((n, dim + 1, form.n_comp), dtype=glob.dtype, device="cuda")))
         if tiles is not None:  # each set's own tile tables, built before the timed graph
             executor.cell_tiles(sets[-1][0], dim, tiles.tile_cells)

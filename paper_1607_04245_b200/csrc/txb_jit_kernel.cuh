@@ -231,18 +231,20 @@ __device__ __forceinline__ void warp_slice(const Tabulation<real>& tab, const re
 #pragma unroll
       for (int j = 0; j < NAUX; ++j) a[j] = s_aux[cell * NAUX + j];
     } else if constexpr (AUXM == 2) {
+      // the cell's nodal row once, vectorised (conflict-free for 32/96-byte rows)
+      real av[NB * NAS];
+      load_row_rot<real, NB * NAS, VEC>(s_aux + cell * AUXW, av, lane);
 #pragma unroll
       for (int b = 0; b < NB; ++b)
 #pragma unroll
-        for (int j = 0; j < NAUX; ++j) a[j] = add(a[j], mul(s_aux[(cell * NB + b) * NAUX + j], tab.B[q * NB + b]));
+        for (int j = 0; j < NAUX; ++j) a[j] = add(a[j], mul(av[b * NAUX + j], tab.B[q * NB + b]));
       if constexpr (GRAD_A) {
 #pragma unroll
         for (int b = 0; b < NB; ++b)
 #pragma unroll
           for (int j = 0; j < NAUX; ++j)
 #pragma unroll
-            for (int k = 0; k < D; ++k)
-              gradA[j][k] = add(gradA[j][k], mul(s_aux[(cell * NB + b) * NAUX + j], tr[b][k]));
+            for (int k = 0; k < D; ++k) gradA[j][k] = add(gradA[j][k], mul(av[b * NAUX + j], tr[b][k]));
       }
     }
 

@@ -320,7 +320,7 @@ def time_mesh(name, steps, warmup, n_sets_min=4, given_geometry=False, tiled=Tru
     if tiled:
         from paper_1607_04245_b200 import executor
 
-        tiles = executor.cell_tiles(cells0, dim, executor.default_tile_cells(dim, 1))
+        tiles = executor.cell_tiles(cells0, dim, executor.default_tile_cells(dim, 1, given_geometry, s))
         # streamed per cell: local indices + the tile record instead of the int64 connectivity
         per_cell += 4 * tiles.local_bytes + tiles.vrec * 4 / tiles.tile_cells - (dim + 1) * 8
     n_sets = max(n_sets_min, -(-3 * L2_BYTES // int(per_cell * n)) + 1)

@@ -449,7 +449,8 @@ def _jit_mesh(kernel, mesh: Mesh, tab: Tabulation, rule: QuadratureRule, form: P
         bad = None
     if n > 0 and _tiled_enabled(mesh, rule):
         # per-tile vertex tables (the tiled kernel's design, run-time compiled form)
-        tiles = cell_tiles(cells_dev, mesh.dim, default_tile_cells(mesh.dim, rule.n_q))
+        tiles = cell_tiles(cells_dev, mesh.dim, default_tile_cells(mesh.dim, rule.n_q, inv is not None,
+                                                                   np.dtype(dt).itemsize))
         rc = _lib.lib().txb_jit_integrate_mesh_tiled(
             ctypes.c_void_p(kernel.handle), n, mesh.n_vertices, B.ctypes.data, D.ctypes.data, W.ctypes.data,
             verts_dev.data_ptr(), tiles.tile_cells, tiles.records.data_ptr(), tiles.vrec, tiles.local.data_ptr(),
@@ -525,16 +526,21 @@ _TILE_CACHE: dict = {}
 _TILE_CACHE_SIZE = 32
 
 
-def default_tile_cells(dim: int, n_q: int) -> int:
+def default_tile_cells(dim: int, n_q: int, given_geometry: bool = False, dtype_bytes: int = 8) -> int:
     """Cells per tile (= per batch) of the tiled kernel: 3D 128 (midpoint) / 64
     (two points), 2D 192 / 96 -- multiples of n_b * n_q and of the warp slice
-    32 / n_q, at most 6 slices (4-6 consumer warps).  TXB_TILE_CELLS overrides."""
+    32 / n_q, at most 6 slices (4-6 consumer warps).  The caller's float64
+    geometry (80 / 40 B per cell streamed with the batch) runs best on half
+    those tiles at the midpoint rule (3D var-coef 25.7 -> 23.4 us, 2D
+    elasticity 21.2 -> 19.6 us at 2^20 cells; profiles/r2_tiled.md).
+    TXB_TILE_CELLS overrides."""
     env = os.environ.get("TXB_TILE_CELLS")
     if env:
         return int(env)
+    half = given_geometry and dtype_bytes == 8 and n_q == 1
     if dim == 3:
-        return 128 if n_q == 1 else 64
-    return 192 if n_q == 1 else 96
+        return (64 if half else 128) if n_q == 1 else 64
+    return (96 if half else 192) if n_q == 1 else 96
 
 
 def cell_tiles(cells_dev, dim: int, tile_cells: int) -> CellTiles:
@@ -616,7 +622,7 @@ def integrate_mesh(mesh: Mesh, layout: FieldLayout, tab: Tabulation, rule: Quadr
     ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
     tiles = None
     if n > 0 and _tiled_enabled(mesh, rule):
-        tiles = cell_tiles(C, mesh.dim, default_tile_cells(mesh.dim, rule.n_q))
+        tiles = cell_tiles(C, mesh.dim, default_tile_cells(mesh.dim, rule.n_q, inv is not None, dt.itemsize))
     if tiles is not None:
         # (geometry +) gather from per-tile vertex tables (csrc/txb_integrate_tiled.cu)
         rc = _lib.lib().txb_integrate_mesh_tiled(

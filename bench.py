@@ -57,6 +57,16 @@ VARIANTS = ["3d_varcoef_f32", "2d_varcoef_f64", "2d_varcoef_f32", "2d_elasticity
             "3d_elasticity_f64", "3d_elasticity_f32", "2d_varcoef_f64_65536"]
 
 
+def nccl_debug_env():
+    """Communicator-init lines of NCCL (ranks, devices, NVLS / P2P transport) for
+    the N > 1 runs, on STDERR: NCCL logs to stdout unless told otherwise, and
+    stdout is the one JSON line.  A caller's own NCCL_DEBUG setting wins."""
+    if "NCCL_DEBUG" not in os.environ:
+        os.environ["NCCL_DEBUG"] = "INFO"
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+
+
 def peaks():
     p = REPO / "MEASURED_PEAKS.json"
     if p.exists():
@@ -961,8 +971,7 @@ def main():
         if dist_backend == "nccl":
             # communicator init lines (ranks, devices, NVLS/P2P transport) on stderr; the
             # hot path itself runs no collective -- only the max-over-ranks time reduction
-            os.environ.setdefault("NCCL_DEBUG", "INFO")
-            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            nccl_debug_env()
             dist.init_process_group("nccl", device_id=torch.device("cuda", device))
             if rank == 0:
                 print(f"[bench] nccl process group: world {world}, rank 0 on cuda:{device}", file=sys.stderr,

@@ -67,3 +67,24 @@ def test_torchrun_two_ranks_reference_arm():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(300)
+def test_nccl_init_logs_stay_off_stdout():
+    """bench.py's N > 1 runs turn on NCCL's init log (NCCL_DEBUG=INFO) for the
+    communicator evidence; NCCL writes it to stdout by default, and the driver
+    reads stdout as the one JSON line.  A one-rank NCCL group (the only NCCL
+    group one B200 allows) with bench.nccl_debug_env(): the INIT lines land on
+    stderr, stdout holds only what the process prints itself."""
+    code = ("import os, sys, torch, torch.distributed as dist; sys.path.insert(0, '.'); import bench; "
+            "bench.nccl_debug_env(); torch.cuda.set_device(0); "
+            "dist.init_process_group('nccl', rank=0, world_size=1, device_id=torch.device('cuda', 0)); "
+            "t = torch.ones(1, device='cuda'); dist.all_reduce(t); torch.cuda.synchronize(); "
+            "dist.destroy_process_group(); print('{\"ok\": 1}')")
+    env = {k: v for k, v in os.environ.items() if not k.startswith("NCCL_DEBUG")}
+    env.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    p = subprocess.run([sys.executable, "-c", code], cwd=REPO, env=env, capture_output=True, text=True, timeout=280)
+    assert p.returncode == 0, p.stderr[-4000:]
+    assert p.stdout.strip() == '{"ok": 1}', p.stdout[-2000:]
+    assert "NCCL INFO" in p.stderr

@@ -680,7 +680,9 @@ class ResidualGraph:
     ``graph(coeffs_global)`` -> the residual, a CUDA tensor owned by the graph
     and overwritten by the next call (pass ``out=`` to copy it out).
     ``coeffs_global``: CUDA tensor or numpy array of layout.global_size(mesh)
-    entries (held in float64, cast to the run dtype inside the graph).
+    entries (held in float64, cast to the run dtype inside the graph).  A
+    solver that writes the graph's own input buffer ``graph.glob`` in place
+    calls ``graph()`` (or passes ``graph.glob``): no copy, one replay.
     One caller at a time: the input and residual buffers are the graph's own
     (not thread-safe; replays are ordered on the caller's current stream)."""
 
@@ -730,15 +732,18 @@ class ResidualGraph:
         self._keep = [cells_dev, verts_dev, _incidence_for(mesh, cells_dev),
                       [t for k, t in _TILE_CACHE.items() if lo <= k[0] < hi]]
 
-    def __call__(self, coeffs_global, out=None):
+    def __call__(self, coeffs_global=None, out=None):
         torch = _torch()
-        if isinstance(coeffs_global, np.ndarray) or not hasattr(coeffs_global, "is_cuda"):
-            src = torch.from_numpy(np.ascontiguousarray(coeffs_global, dtype=np.float64))
-        else:
-            src = coeffs_global
-        if int(src.numel()) != self.n:
-            raise ShapeError(f"global vector has {src.numel()} entries, expected {self.n}")
-        self.glob.copy_(src.reshape(-1), non_blocking=False)
+        if coeffs_global is not None and not (hasattr(coeffs_global, "data_ptr") and
+                                              coeffs_global.data_ptr() == self.glob.data_ptr()):
+            if isinstance(coeffs_global, np.ndarray) or not hasattr(coeffs_global, "is_cuda"):
+                src = torch.from_numpy(np.ascontiguousarray(coeffs_global, dtype=np.float64))
+            else:
+                src = coeffs_global
+            if int(src.numel()) != self.n:
+                raise ShapeError(f"global vector has {src.numel()} entries, expected {self.n}")
+            self.glob.copy_(src.reshape(-1), non_blocking=False)
+        # (None, or the graph's own input buffer: the caller wrote graph.glob in place -- no copy)
         self.graph.replay()
         if out is not None:
             out.copy_(self.residual)

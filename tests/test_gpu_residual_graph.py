@@ -53,6 +53,11 @@ def test_graph_replays_match_eager(dim, n, factory, aux_space, dtype, two_point)
     out = torch.empty_like(g.residual)
     g(gh, out=out)
     assert bitwise_equal(out.cpu().numpy(), want)
+    # in place: the solver writes graph.glob and replays without a copy
+    g.glob.copy_(torch.from_numpy(gh * 0.5))
+    want, _ = txb.integrate_transposed(mesh, layout, tab, rule, form, gh * 0.5, aux, **kw)
+    assert bitwise_equal(g().cpu().numpy(), want)
+    assert bitwise_equal(g(g.glob).cpu().numpy(), want)
 
 
 def test_graph_given_geometry_and_nonstandard_tables():

@@ -162,3 +162,34 @@ def test_reference_decomposition_is_a_model_parameter(paper, monkeypatch):
     elem = oracle.integrate(1, 1, tab.basis, tab.basis_der, rule.weights, inv, det,
                             oracle.gather(mesh.cells, glob, 1), kappa.values)
     assert bitwise_equal(res, oracle.scatter_add(mesh.cells, elem, mesh.n_vertices))
+
+
+def test_integrate_transposed_from_threads():
+    """The reference's callers run the lane from a thread pool (executor.py:228-239);
+    here eight threads share the process's mesh / incidence / tile caches and
+    the pinned staging of numpy inputs, each integrating its own mesh and
+    coefficient vector (numpy in, numpy out; in-kernel and given geometry,
+    f64 and f32): every residual bit-identical to the oracle's."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    jobs = []
+    for k in range(16):
+        dim = 2 if k % 2 else 3
+        size = 30 if k == 0 else (40 if dim == 2 else 8) + k % 3  # k = 0: 162,000 tets
+        form, mesh, layout, rule, tab, geom, coeffs = make_problem(dim, FORMS["poisson_varcoef"], size, seed=k)
+        # >= 1 MiB of kappa for some: the pinned-staging H2D path
+        aux = txb.CellAux("p0", np.random.default_rng(100 + k).uniform(0.5, 1.5, (mesh.n_cells, 1)))
+        jobs.append((form, mesh, layout, rule, tab, geom, coeffs, aux, "f32" if k % 4 == 3 else "f64", k % 3 == 0))
+
+    def run(job):
+        form, mesh, layout, rule, tab, geom, coeffs, aux, dtype, given = job
+        res, trace = txb.integrate_transposed(mesh, layout, tab, rule, form, coeffs, aux, n_bl=4, n_cb=2,
+                                              dtype=dtype, cell_geom=geom if given else None)
+        return res, trace
+
+    with ThreadPoolExecutor(8) as ex:
+        results = list(ex.map(run, jobs * 2))
+    for (form, mesh, layout, rule, tab, geom, coeffs, aux, dtype, _), (res, trace) in zip(jobs * 2, results):
+        npdt = np.float32 if dtype == "f32" else np.float64
+        span = trace.geom.n_chunks * trace.geom.n_chunk
+        assert bitwise_equal(res, oracle_residual(mesh, layout, tab, rule, form, geom, coeffs, aux, npdt, span))

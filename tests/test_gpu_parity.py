@@ -7,6 +7,7 @@ north_star tolerances (rel 1e-5 f32, 1e-12 f64) are asserted as well.
 """
 
 import hashlib
+import os
 
 import numpy as np
 import pytest
@@ -342,7 +343,7 @@ def test_back_to_back_launches_see_each_others_writes():
 from hypothesis import HealthCheck, given, settings, strategies as st  # noqa: E402
 
 
-@settings(max_examples=120, deadline=None, suppress_health_check=list(HealthCheck))
+@settings(max_examples=int(os.environ.get("TXB_HYPOTHESIS_EXAMPLES", 120)), deadline=None, suppress_health_check=list(HealthCheck))
 @given(dim=st.integers(2, 3), form=st.sampled_from([(0, 0), (1, 1), (1, 2), (2, 0)]), n_q=st.integers(1, 8),
        n=st.integers(0, 3000), dtype=st.sampled_from(["f64", "f32"]), tables=st.sampled_from(["p1", "random"]),
        n_bl=st.sampled_from([0, 1, 3, 8, 17]), n_cb=st.sampled_from([0, 1, 5]), offset=st.sampled_from([0, 0, 1]),

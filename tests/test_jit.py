@@ -8,6 +8,7 @@ GPU tests: element vectors bit-identical to the reference's python lane
 seeded inputs; the shipped forms compiled at run time equal the ahead-of-time
 kernel bit for bit; the mesh-level driver routes user forms through it."""
 
+import os
 import shutil
 import subprocess
 
@@ -358,7 +359,7 @@ from hypothesis import HealthCheck, given, settings, strategies as st  # noqa: E
 
 
 @pytest.mark.gpu
-@settings(max_examples=40, deadline=None, suppress_health_check=list(HealthCheck))
+@settings(max_examples=int(os.environ.get("TXB_HYPOTHESIS_EXAMPLES", 40)), deadline=None, suppress_health_check=list(HealthCheck))
 @given(name=st.sampled_from(SPECS), dim=st.integers(2, 3), n_q=st.integers(1, 3), n=st.integers(0, 2500),
        dtype=st.sampled_from([np.float64, np.float32]), n_bl=st.sampled_from([0, 1, 5]), seed=st.integers(0, 999))
 def test_jit_random_problems_bitwise(name, dim, n_q, n, dtype, n_bl, seed):

@@ -247,6 +247,9 @@ __device__ __forceinline__ void affine_inverse(const double (&X)[D + 1][D], doub
 #define TXB_DD_RECIPROCAL 1
 #endif
 __device__ __forceinline__ bool dd_range_bad(double x) {
+#ifdef TXB_DIAG_NO_NUM_CHECK  // diagnostic builds only (unsafe): what the per-numerator test costs
+  return false;
+#endif
   const unsigned hi = (unsigned)__double2hiint(x) & 0x7fffffffu, lo = (unsigned)__double2loint(x);
   return (hi - 0x20B00000u > 0x3E800000u) & ((hi | lo) != 0u);
 }

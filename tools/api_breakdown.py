@@ -1,3 +1,7 @@
+"""Where the mesh-level call from numpy spends its time (1 M-tet 3D var-coef f64):
+the whole integrate_transposed call, the H2D of kappa (pageable vs pinned staging),
+the coefficient H2D, the residual D2H, the device-resident call, and a cProfile of
+the Python side.  Run from the repo root: python tools/api_breakdown.py"""
 import sys, time, json
 sys.path.insert(0, '.')
 import numpy as np, torch

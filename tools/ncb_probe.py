@@ -1,3 +1,6 @@
+"""The reference's (N_bl, N_cb) decompositions run as given vs the tuned default on
+the device (graph-timed integrate_cells chains, 2^20 cells): profiles/r2_decomposition.md.
+Run from the repo root: python tools/ncb_probe.py"""
 import sys, json, os
 sys.path.insert(0, '.')
 import numpy as np, torch, bench

@@ -1,3 +1,6 @@
+"""ResidualGraph per form on the ~1 M-tet 3D Kuhn mesh (an NVRTC user form with f0,
+two P1 fields and grad a; the ahead-of-time var-coef form): ms per residual.
+Run from the repo root: python tools/residual_graph_forms.py"""
 import sys, time, json
 sys.path.insert(0, '.')
 import numpy as np, torch

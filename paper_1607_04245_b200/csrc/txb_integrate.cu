@@ -378,6 +378,13 @@ static bool pick_nq(const Config& c, bool std_tab, KernelInfo& k) {
   return false;
 }
 
+// 2D f32 elasticity, launch-sized problems: 4 consumer warps looping over the
+// 9 slices of a 288-cell batch beat 9 warps (2^20 cells 11.9 -> 11.7 us; at
+// 2^22 cells and above the wide CTA stays faster; profiles/r2bd_bounds.md).
+static void size_tuning(const Config& c, int64_t n_cells, KernelInfo& k) {
+  if (c.form == 2 && c.dim == 2 && c.dtype == 4 && n_cells < ((int64_t)1 << 22)) k.max_warps = 4;
+}
+
 static bool pick_kernel(const Config& c, bool std_tab, KernelInfo& k) {
   if (env_int("TXB_DISABLE_STD", 0)) std_tab = false;
   if (c.dtype == 4) return c.dim == 2 ? pick_nq<float, 2>(c, std_tab, k) : pick_nq<float, 3>(c, std_tab, k);
@@ -456,6 +463,7 @@ int integrate_device(const Config& c, int n_b, int64_t n_cells, const void* basi
     set_error("no kernel instantiation for this configuration");
     return TXB_E_UNSUPPORTED;
   }
+  size_tuning(c, n_cells, k);
   Geometry g;
   rc = compute_geometry(c, k, n_cells, n_bl, n_cb, true, g);
   if (rc) return rc;
@@ -840,6 +848,7 @@ extern "C" int txb_launch_config(int form_code, int aux_mode, int dtype_bytes, i
   if (rc) return rc;
   KernelInfo k;  // reports the standard-P1-table kernel's geometry
   if (!pick_kernel(c, true, k)) return TXB_E_UNSUPPORTED;
+  size_tuning(c, n_cells, k);
   int ndev = 0;
   const bool have_dev = cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0;
   if (!have_dev) cudaGetLastError();
